@@ -1,0 +1,188 @@
+/*
+ * rapid.h — C ABI of the B200-native RAPID / CTFTPS superpixel refinement library.
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, "P:n" = line n):
+ *   The coarse-to-fine topology-preserving superpixel refinement (CTFTPS, §2.1)
+ *   as modified by RAPID (§3): superpixels start as a regular grid (RAPID l.1,
+ *   P:124); at every block stage (RAPID l.5-8) each boundary block may be
+ *   relabelled to a 4-neighbouring superpixel (Eq. 3) under the energy of Eq. 1
+ *   (colour + lambda_pos position + lambda_b boundary length, Eq. 2) if the move
+ *   keeps every superpixel 4-connected (E_topo) and, in the size-regularity modes,
+ *   the superpixel above l*InitSize (E_size P:68 / §3.1); undersized superpixels are
+ *   merged into the contiguous superpixel of least merged energy within u*InitSize
+ *   (Eqs. 4-5); after the coarsest stage a classifier (Eq. 6) gates
+ *   which superpixels are refined later (Eq. 7); coarsest-level
+ *   statistics are reused at finer levels (Eq. 8).
+ *   The exact deterministic schedule (2x2 parity-coloured sweeps, frozen per-phase
+ *   fixed-point means, all-or-nothing size budget, ordered merge rounds) and every reading
+ *   of an ambiguous passage are listed in DESIGN.md §2.  Output label maps are bit-exact
+ *   with the CPU oracle (oracle/) under those readings.
+ *
+ * Conventions
+ *   - All entry points return int status (RAPID_OK = 0, negative = error, see below);
+ *     nothing throws across the ABI; argument validation happens before any launch.
+ *   - Device pointers are CUDA device addresses on the ctx's device.  Host pointers are
+ *     ordinary (preferably pinned) host memory.  `stream` is a cudaStream_t passed as
+ *     void* (NULL = legacy default stream).
+ *   - Ownership: images and label buffers belong to the caller and must stay valid until
+ *     the stream work completes; the ctx owns every internal buffer.
+ *   - Threading: one ctx per concurrently used stream; calls on one ctx are not reentrant.
+ */
+#ifndef RAPID_H
+#define RAPID_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RAPID_MAX_STAGES 12
+#define RAPID_MAX_SWEEPS 64
+#define RAPID_MAX_PROTO 4
+#define RAPID_NCNT 6
+
+/* status codes */
+#define RAPID_OK 0
+#define RAPID_E_ARG (-1)       /* null pointer, bad sizes, bad stage list, l>=1, u<=1, ... */
+#define RAPID_E_CAPACITY (-2)  /* B*H*W or B*M exceeds the capacity given to rapid_init */
+#define RAPID_E_RANGE (-3)     /* values that could overflow the integer energy parts */
+#define RAPID_E_CUDA (-4)      /* a CUDA call failed; rapid_last_error() has the message */
+#define RAPID_E_OOM (-5)       /* device allocation failed */
+#define RAPID_E_INTEGRITY (-6) /* RECOUNT mode found reused sums != recount (never expected) */
+#define RAPID_E_STATE (-7)     /* stats/profile requested before any segmentation */
+
+/* size_mode: how E_size is handled */
+#define RAPID_SIZE_NONE 0  /* lambda_s = 0: no size limit (CTFTPS case 1) */
+#define RAPID_SIZE_HARD 1  /* lambda_s = inf: moves below l*InitSize rejected (case 2) */
+#define RAPID_SIZE_MERGE 2 /* RAPID regularity optimisation: merge instead (§3.1) */
+
+/* mask_rule: which blocks are refined after the coarsest stage (RAPID l.3-4, l.14) */
+#define RAPID_MASK_OFF 0   /* everything is refined (CTFTPS) */
+#define RAPID_MASK_CLASS 1 /* superpixels with y=+1 (config text: ROI-like colour) */
+#define RAPID_MASK_BSP 2   /* "boundary superpixels": a 4-adjacent superpixel of the other class */
+#define RAPID_MASK_EQ7 3   /* block-level Eq. 7: a neighbour with another label and another class */
+
+/* stats_mode */
+#define RAPID_STATS_REUSE 0   /* RAPID: coarsest-level sums reused (Eq. 8, exact here) */
+#define RAPID_STATS_RECOUNT 1 /* multi-scale CTFTPS: recount at every stage (checked equal) */
+
+/* per-phase counters (rapid_run_info.phase) */
+#define RAPID_C_CAND 0    /* gated boundary blocks of the phase colour */
+#define RAPID_C_TOPO 1    /* ... that passed the simple-point test */
+#define RAPID_C_PROP 2    /* proposals: dE<0 and the single-move size gate passed */
+#define RAPID_C_SIZEREJ 3 /* desired moves rejected by the single-move size gate */
+#define RAPID_C_COMMIT 4  /* committed moves */
+#define RAPID_C_COMMREJ 5 /* proposals dropped by the all-or-nothing size budget */
+
+typedef struct rapid_ctx rapid_ctx; /* opaque; owns all device workspace */
+
+/* Parameters of one segmentation call.  Integers only, so results are bit-reproducible. */
+typedef struct {
+  uint32_t struct_size;      /* = sizeof(rapid_params) (ABI check) */
+  uint32_t batch;            /* B >= 1 independent images of H x W (A27) */
+  uint32_t n_superpixels;    /* M per image; grid r x c = M with the squarest cells */
+  uint32_t n_stages;         /* 1..RAPID_MAX_STAGES */
+  uint32_t block_size[RAPID_MAX_STAGES]; /* descending, 1..64, each divides the previous;
+                                            the last is the final grain (Table 1) */
+  uint32_t sweeps;           /* parity sweeps per stage, 0..RAPID_MAX_SWEEPS (A5, A25) */
+  int64_t lambda_pos_q16;    /* lambda_pos in Q16.16, 0..2^31-1 */
+  int64_t lambda_b_q16;      /* lambda_b in Q16.16 per ordered pixel pair, 0..2^31-1 (A3) */
+  uint32_t size_mode;        /* RAPID_SIZE_* */
+  uint32_t l_num, l_den;     /* lower size bound l = l_num/l_den < 1 (default 1/4) */
+  uint32_t u_num, u_den;     /* upper size bound u = u_num/u_den > 1 (Eq. 5; default 3/2) */
+  uint32_t mask_rule;        /* RAPID_MASK_* */
+  uint32_t n_proto;          /* 1..4 when mask_rule != OFF */
+  uint8_t proto_rgb[RAPID_MAX_PROTO][3]; /* prototypes of h_theta (A21) */
+  uint8_t pad_[4];
+  int64_t tau2;              /* y=+1 iff min_k ||c - proto_k||^2 <= tau2 (Eq. 6; intensity^2) */
+  uint32_t stats_mode;       /* RAPID_STATS_* */
+  uint32_t pad2_;
+} rapid_params;
+
+/* Per-superpixel result, index img*M + local id. */
+typedef struct {
+  int64_t n, sum_r, sum_g, sum_b, sum_x, sum_y; /* exact integer sums (x = column) */
+  double mean_r, mean_g, mean_b, mean_x, mean_y; /* sum / n (0 when n == 0) */
+  int32_t init_size;                            /* InitSize (cell area) */
+  int8_t alive, active, y;                      /* y in {-1,+1}, 0 = not predicted */
+  int8_t pad_;
+} rapid_sp_stat;
+
+typedef struct {
+  int32_t status;            /* status of the last segmentation (deferred errors) */
+  uint32_t batch, H, W, n_superpixels, n_stages, sweeps;
+  uint32_t grid_rows, grid_cols;
+  uint32_t stage_nbx[RAPID_MAX_STAGES], stage_nby[RAPID_MAX_STAGES];
+  uint64_t stage_tiles[RAPID_MAX_STAGES];        /* tiles of the stage map */
+  uint64_t stage_active_tiles[RAPID_MAX_STAGES]; /* tiles on the worklist */
+  uint64_t stage_victims[RAPID_MAX_STAGES];      /* victims at the stage's merge round */
+  uint64_t stage_merges[RAPID_MAX_STAGES];
+  uint64_t stage_sweeps_run[RAPID_MAX_STAGES];   /* sweeps actually executed (exact early exit) */
+  uint64_t alive, active;                        /* after the run */
+  uint64_t phase[RAPID_MAX_STAGES][RAPID_MAX_SWEEPS][4][RAPID_NCNT]; /* RAPID_C_* */
+} rapid_run_info;
+
+/* Kernel timing (profiling mode): per kernel class and stage. */
+#define RAPID_K_PYRAMID 0
+#define RAPID_K_SNAPSHOT 1
+#define RAPID_K_PROPOSE 2
+#define RAPID_K_COMMIT 3
+#define RAPID_K_MERGE 4
+#define RAPID_K_PREDICT 5
+#define RAPID_K_TRANSITION 6
+#define RAPID_K_FINAL 7
+#define RAPID_K_PHASESET 8 /* snapshot+propose+commit of every phase of the stage, as one interval */
+#define RAPID_NK 9
+typedef struct {
+  uint64_t launches[RAPID_NK][RAPID_MAX_STAGES];
+  double ms[RAPID_NK][RAPID_MAX_STAGES];
+  uint64_t total_launches; /* every kernel of the last segmentation */
+} rapid_profile;
+
+/* Create a context on CUDA device `device`, sized for at most `max_pixels_total` = B*H*W
+ * pixels and `max_superpixels_total` = B*M superpixels per call.  *out = NULL on error. */
+int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total,
+               uint64_t max_superpixels_total);
+
+/* Segment image (device, u8 [B][H][W][3], RGB, row-major) into labels_out (device, int32
+ * [B][H][W], per-image local ids in [0, M); merged-away ids are absent).  Only enqueues
+ * work on `stream`; returns after validation and launch. */
+int rapid_segment(rapid_ctx *ctx, const uint8_t *image, int32_t H, int32_t W,
+                  const rapid_params *params, int32_t *labels_out, void *stream);
+
+/* Same, end to end from host buffers: copies image_host to the device, segments, copies
+ * the labels back into labels_host, and synchronises `stream` before returning. */
+int rapid_segment_host(rapid_ctx *ctx, const uint8_t *image_host, int32_t H, int32_t W,
+                       const rapid_params *params, int32_t *labels_host, void *stream);
+
+/* Synchronise the last segmentation's stream and copy per-superpixel stats (up to
+ * `capacity` entries; out_host may be NULL) and run info (may be NULL) to the host.
+ * Returns the deferred status of that segmentation (e.g. RAPID_E_INTEGRITY). */
+int rapid_stats(rapid_ctx *ctx, rapid_sp_stat *out_host, uint64_t capacity,
+                rapid_run_info *info_host);
+
+/* Profiling: when enabled, CUDA events bracket every kernel class per stage. */
+int rapid_set_profiling(rapid_ctx *ctx, int enable);
+int rapid_get_profile(rapid_ctx *ctx, rapid_profile *out_host); /* synchronises */
+
+void rapid_free(rapid_ctx *ctx); /* synchronises first; NULL is a no-op */
+const char *rapid_status_string(int status);
+const char *rapid_last_error(const rapid_ctx *ctx);
+
+/* ---- debug (parity bisection against the oracle; not for production use) ---------- */
+#define RAPID_STOP_NONE 0
+#define RAPID_STOP_PHASE 1        /* after the commit of (stage, sweep, phase) */
+#define RAPID_STOP_STAGE_START 2  /* after the transition into `stage` */
+#define RAPID_STOP_AFTER_MERGE 3  /* after the merge round of `stage` */
+#define RAPID_STOP_AFTER_PREDICT 4
+/* The next segmentation stops at the given point (labels_out is then undefined);
+ * rapid_debug_map copies the stage map [B][nby][nbx] there to the host. */
+int rapid_debug_stop(rapid_ctx *ctx, int kind, int stage, int sweep, int phase);
+int rapid_debug_map(rapid_ctx *ctx, int32_t *host, uint64_t capacity, int32_t *nbx,
+                    int32_t *nby);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAPID_H */

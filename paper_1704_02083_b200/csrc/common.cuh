@@ -1,0 +1,138 @@
+// common.cuh — device-side data layout shared by the RAPID kernels (sm_100a).
+// Product code: never includes or links anything under oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rapid {
+
+constexpr int FRAC = 8;          // F: fractional bits of the snapshot means (DESIGN §2 A24)
+constexpr int TX = 64;           // sweep tile width in blocks
+constexpr int TY = 16;           // sweep tile height in blocks
+constexpr int PROP_THREADS = 256;// one candidate per thread: (TX/2)*(TY/2) = 256
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int NCNT = 6;          // per-phase counters (RAPID_C_*)
+constexpr int MAXS = 12;
+constexpr int MAXSW = 64;
+
+// stats record of a superpixel: 8 x int64 (n, r, g, b, x, y, pad, pad); 64-B aligned
+constexpr int SUMW = 8;
+
+// Snapshot record: one 32-B sector per superpixel, refreshed before every phase
+// (frozen per-phase means, DESIGN §2 A4).  cq/mu are round-half-up(2^F * mean).
+struct __align__(16) Rec {
+  int32_t mux, muy;   // position means, 2^F units (< 2^24)
+  uint32_t cq01;      // cq_r | cq_g << 16 (each <= 255*2^8)
+  uint32_t cq2f;      // cq_b | flags << 16
+  int32_t n;          // size at snapshot
+  int32_t init;       // InitSize
+  int32_t pad0, pad1;
+};
+// flags
+constexpr uint32_t F_ALIVE = 1u, F_ACTIVE = 2u;
+// y is stored as (y + 1) in bits 2..3
+
+struct StageDev {
+  int32_t nbx, nby, b;
+  int32_t tiles_x, tiles_y;      // sweep tiles per image
+  const int32_t *xs, *ys;        // block boundaries (nbx+1, nby+1)
+  const int32_t *px, *py;        // parent block index in stage s-1 (s > 0)
+  const int32_t *cxs, *cys;      // first child index in stage s+1 (nbx+1, nby+1)
+  const uint64_t *bsum;          // packed colour sums r | g<<21 | b<<42 (b > 1), else null
+  int32_t *map;                  // stage label map [B][nby][nbx], per-image local ids
+};
+
+struct SpDev {
+  unsigned long long *sums;  // [K][SUMW]
+  Rec *rec;                  // [K]
+  int32_t *init;             // [K]
+  uint8_t *alive, *active;   // [K]
+  int8_t *y;                 // [K]
+  uint8_t *victim;           // [K]
+  int32_t *out;              // [K] proposed outflow of the current phase
+  uint32_t *dirty;           // [K] stamp of the last dirty-list insertion
+  int32_t *remap;            // [K]
+};
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Warp-aggregated delta update of the six int64 sums of superpixel `key` (north star (d)):
+// lanes with the same key are reduced with shuffles and one lane issues the atomics.
+// Integer atomics are order-independent, so the result is deterministic.
+__device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[6], bool negate,
+                                         unsigned long long *sums, uint32_t *dirty, uint32_t stamp,
+                                         int32_t *dlist, unsigned int *dcount) {
+  unsigned pend = __ballot_sync(FULL, valid);
+  const int lane = lane_id();
+  while (pend) {
+    const int src = __ffs(pend) - 1;
+    const int k = __shfl_sync(FULL, key, src);
+    const bool in = valid && key == k;
+    const unsigned grp = __ballot_sync(FULL, in);
+#pragma unroll
+    for (int f = 0; f < 6; f++) {
+      long long v = in ? d[f] : 0;
+      v = warp_sum_ll(v);
+      if (lane == src) atomicAdd(&sums[(size_t)k * SUMW + f], (unsigned long long)(negate ? -v : v));
+    }
+    if (lane == src && dirty != nullptr) {
+      if (atomicExch(&dirty[k], stamp) != stamp) {
+        unsigned pos = atomicAdd(dcount, 1u);
+        dlist[pos] = k;
+      }
+    }
+    pend &= ~grp;
+  }
+}
+
+// Warp-aggregated int32 add (proposal outflow per source superpixel).
+__device__ __forceinline__ void agg_add_i32(bool valid, int key, int v, int32_t *arr) {
+  unsigned pend = __ballot_sync(FULL, valid);
+  const int lane = lane_id();
+  while (pend) {
+    const int src = __ffs(pend) - 1;
+    const int k = __shfl_sync(FULL, key, src);
+    const bool in = valid && key == k;
+    const unsigned grp = __ballot_sync(FULL, in);
+    int s = in ? v : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if (lane == src) atomicAdd(&arr[k], s);
+    pend &= ~grp;
+  }
+}
+
+// Block data of a block at stage `st`: n, colour sums, position sums (x = column).
+// Positions are closed-form sums over the block rectangle at full resolution (Eq. 8 exact).
+__device__ __forceinline__ void block_data_blk(const StageDev &st, int img, int gx, int gy,
+                                               long long d[6]) {
+  const long long x0 = st.xs[gx], x1 = st.xs[gx + 1];
+  const long long y0 = st.ys[gy], y1 = st.ys[gy + 1];
+  const long long w = x1 - x0, h = y1 - y0;
+  const uint64_t pk = st.bsum[((size_t)img * st.nby + gy) * st.nbx + gx];
+  d[0] = w * h;
+  d[1] = (long long)(pk & 0x1FFFFFull);
+  d[2] = (long long)((pk >> 21) & 0x1FFFFFull);
+  d[3] = (long long)(pk >> 42);
+  d[4] = h * ((w * (2 * x0 + w - 1)) / 2);
+  d[5] = w * ((h * (2 * y0 + h - 1)) / 2);
+}
+
+__device__ __forceinline__ void block_data_pix(const uint8_t *image, int H, int W, int img, int gx,
+                                               int gy, long long d[6]) {
+  const uint8_t *p = image + (((size_t)img * H + gy) * W + gx) * 3;
+  d[0] = 1;
+  d[1] = p[0];
+  d[2] = p[1];
+  d[3] = p[2];
+  d[4] = gx;
+  d[5] = gy;
+}
+
+}  // namespace rapid

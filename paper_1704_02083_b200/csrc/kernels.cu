@@ -1,0 +1,1020 @@
+// kernels.cu — the RAPID / CTFTPS refinement hot path on sm_100a.
+//
+// Kernel map (SURVEY §2.4 / DESIGN.md §4):
+//   K1 pyramid_leaf/pyramid_up  block-sum pyramid (Eq. 8 exact, A23)
+//   K2 init_sp/init_map0/stats0 grid labels + S_1 (RAPID l.1, l.9-10)
+//   K3 snapshot                 frozen per-phase fixed-point means (RAPID l.18; A4, A24)
+//   K4 propose                  parity-phase boundary sweep: Eq. 1-3, E_topo, Eq. 7 gate, size gate
+//   K5 commit                   all-or-nothing size budget + warp-aggregated stats deltas
+//   K6 merge round              Eqs. 4-5, ordered resolution (A12-A16)
+//   K7 predict                  Eq. 6 + boundary superpixels + active compaction
+//   K8 transition               label mapping to the next stage + active-tile worklist
+//   K9 final                    final grain upsample / pending remap (Table 1 grain)
+#include <cstdio>
+
+#include "kernels.cuh"
+
+namespace rapid {
+
+typedef __int128 i128;
+
+// ------------------------------------------------------------------------------- helpers
+__device__ __forceinline__ bool sweep_skipped(const unsigned long long *prev) {
+  // Exact early exit (DESIGN §2 A25): a sweep with zero commits leaves labels and sums
+  // unchanged, so every later sweep of the stage would repeat it identically.
+  if (prev == nullptr) return false;
+  return (prev[0 * NCNT + 4] + prev[1 * NCNT + 4] + prev[2 * NCNT + 4] + prev[3 * NCNT + 4]) == 0ull;
+}
+
+// Yokoi 4-connectivity number == 1 on the 8-ring (N,NE,E,SE,S,SW,W,NW = bits 0..7):
+// C4 = sum_{k in N,E,S,W} x_k (1 - x_{k+1} x_{k+2})   (E_topo; DESIGN A9)
+__device__ __forceinline__ bool simple_point(unsigned m) {
+  const unsigned r = m | (m << 8);  // ring wrap
+  unsigned c = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    const unsigned xk = (r >> k) & 1u, x1 = (r >> (k + 1)) & 1u, x2 = (r >> (k + 2)) & 1u;
+    c += xk & ~(x1 & x2) & 1u;
+  }
+  return c == 1u;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ------------------------------------------------------------------ K2: initial state
+__global__ void k_init_sp(const InitArgs a) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.K; k += gridDim.x * blockDim.x) {
+    const int local = k % a.M;
+    const int j = local / a.cols, i = local - j * a.cols;
+    a.sp.init[k] = (a.X[i + 1] - a.X[i]) * (a.Y[j + 1] - a.Y[j]);  // InitSize = cell area
+    a.sp.alive[k] = 1;
+    a.sp.active[k] = 1;
+    a.sp.y[k] = 0;
+    a.sp.victim[k] = 0;
+    a.sp.remap[k] = local;
+#pragma unroll
+    for (int f = 0; f < SUMW; f++) a.sp.sums[(size_t)k * SUMW + f] = 0ull;
+  }
+}
+
+// K1: packed colour sums of the finest block stage, by direct summation over each block.
+__global__ void k_pyramid_leaf(const StageDev st, const uint8_t *__restrict__ image, int H, int W,
+                               int B, uint64_t *__restrict__ bsum) {
+  const size_t nper = (size_t)st.nbx * st.nby;
+  const size_t n = nper * B;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const int img = (int)(t / nper);
+    const size_t r = t - (size_t)img * nper;
+    const int gy = (int)(r / st.nbx), gx = (int)(r - (size_t)gy * st.nbx);
+    const int x0 = st.xs[gx], x1 = st.xs[gx + 1], y0 = st.ys[gy], y1 = st.ys[gy + 1];
+    uint32_t sr = 0, sg = 0, sb = 0;
+    for (int y = y0; y < y1; y++) {
+      const uint8_t *row = image + (((size_t)img * H + y) * W) * 3;
+      for (int x = x0; x < x1; x++) {
+        sr += row[3 * x];
+        sg += row[3 * x + 1];
+        sb += row[3 * x + 2];
+      }
+    }
+    bsum[t] = (uint64_t)sr | ((uint64_t)sg << 21) | ((uint64_t)sb << 42);
+  }
+}
+
+// K1: coarser stage from its <= 2x2 children (packed fields never overflow: block <= 64^2).
+__global__ void k_pyramid_up(const StageDev st, const StageDev ch, int B, uint64_t *__restrict__ bsum) {
+  const size_t nper = (size_t)st.nbx * st.nby;
+  const size_t n = nper * B;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const int img = (int)(t / nper);
+    const size_t r = t - (size_t)img * nper;
+    const int gy = (int)(r / st.nbx), gx = (int)(r - (size_t)gy * st.nbx);
+    uint64_t acc = 0;
+    for (int cy = st.cys[gy]; cy < st.cys[gy + 1]; cy++)
+      for (int cx = st.cxs[gx]; cx < st.cxs[gx + 1]; cx++)
+        acc += ch.bsum[((size_t)img * ch.nby + cy) * ch.nbx + cx];
+    bsum[t] = acc;
+  }
+}
+
+__global__ void k_init_map0(const InitArgs a) {
+  const StageDev &st = a.st0;
+  const size_t nper = (size_t)st.nbx * st.nby;
+  const size_t n = nper * a.B;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = t % nper;
+    const int gy = (int)(r / st.nbx), gx = (int)(r - (size_t)gy * st.nbx);
+    st.map[t] = a.celly[gy] * a.cols + a.cellx[gx];  // label j*c + i (RAPID l.1)
+  }
+}
+
+// S_1: per-superpixel int64 sums from the stage-0 blocks (warp-aggregated atomics).
+template <bool PIXEL>
+__global__ void k_stats0(const InitArgs a) {
+  const StageDev &st = a.st0;
+  const size_t nper = (size_t)st.nbx * st.nby;
+  const size_t n = nper * a.B;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t base = blockIdx.x * (size_t)blockDim.x; base < n; base += stride) {
+    const size_t t = base + threadIdx.x;
+    const bool valid = t < n;
+    long long d[6] = {0, 0, 0, 0, 0, 0};
+    int key = 0;
+    if (valid) {
+      const int img = (int)(t / nper);
+      const size_t r = t - (size_t)img * nper;
+      const int gy = (int)(r / st.nbx), gx = (int)(r - (size_t)gy * st.nbx);
+      if (PIXEL) block_data_pix(a.image, a.H, a.W, img, gx, gy, d);
+      else block_data_blk(st, img, gx, gy, d);
+      key = img * a.M + st.map[t];
+    }
+    agg_sums(valid, key, d, false, a.sp.sums, nullptr, 0, nullptr, nullptr);
+  }
+}
+
+// ------------------------------------------------------------------ K3: snapshot
+__device__ __forceinline__ void make_rec(const SpDev &sp, int k) {
+  const unsigned long long *s = sp.sums + (size_t)k * SUMW;
+  const unsigned long long n = s[0];
+  Rec r;
+  r.n = (int32_t)n;
+  r.init = sp.init[k];
+  const uint32_t flags = (uint32_t)sp.alive[k] | ((uint32_t)sp.active[k] << 1) |
+                         ((uint32_t)(sp.y[k] + 1) << 2);
+  uint32_t c0 = 0, c1 = 0, c2 = 0;
+  int32_t mx = 0, my = 0;
+  if (n > 0) {
+    const unsigned long long twon = 2 * n;
+    // round-half-up(2^F S / n) = floor((2^(F+1) S + n) / 2n)  (A24)
+    c0 = (uint32_t)(((s[1] << (FRAC + 1)) + n) / twon);
+    c1 = (uint32_t)(((s[2] << (FRAC + 1)) + n) / twon);
+    c2 = (uint32_t)(((s[3] << (FRAC + 1)) + n) / twon);
+    mx = (int32_t)(((s[4] << (FRAC + 1)) + n) / twon);
+    my = (int32_t)(((s[5] << (FRAC + 1)) + n) / twon);
+  }
+  r.mux = mx;
+  r.muy = my;
+  r.cq01 = c0 | (c1 << 16);
+  r.cq2f = c2 | (flags << 16);
+  r.pad0 = r.pad1 = 0;
+  sp.rec[k] = r;
+}
+
+__global__ void k_snapshot(const SnapArgs a) {
+  const int n = a.list ? (int)*a.count : a.K;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    make_rec(a.sp, a.list ? a.list[i] : i);
+}
+
+// ------------------------------------------------------------------ K4: propose
+struct RecV {
+  long long c0, c1, c2, mx, my;
+};
+__device__ __forceinline__ RecV rec_vals(const Rec &r) {
+  RecV v;
+  v.c0 = r.cq01 & 0xffffu;
+  v.c1 = r.cq01 >> 16;
+  v.c2 = r.cq2f & 0xffffu;
+  v.mx = r.mux;
+  v.my = r.muy;
+  return v;
+}
+
+// 2^(-16) x the oracle's weighted dE (same sign, same order): exact integer Eq. 1 difference
+// of relabelling a pixel set with data d from A to B under the frozen means.
+__device__ __forceinline__ i128 delta_e(const RecV &ra, const RecV &rb, const long long d[6],
+                                        long long dB2, long long lam_pos, long long lam_b) {
+  const long long n = d[0];
+  long long dC = (rb.c0 - ra.c0) * (n * (rb.c0 + ra.c0) - (d[1] << (FRAC + 1))) +
+                 (rb.c1 - ra.c1) * (n * (rb.c1 + ra.c1) - (d[2] << (FRAC + 1)));
+  i128 dCw = (i128)dC + (i128)((rb.c2 - ra.c2) * (n * (rb.c2 + ra.c2) - (d[3] << (FRAC + 1))));
+  const long long dP = (rb.mx - ra.mx) * (n * (rb.mx + ra.mx) - (d[4] << (FRAC + 1))) +
+                       (rb.my - ra.my) * (n * (rb.my + ra.my) - (d[5] << (FRAC + 1)));
+  return (dCw << 16) + (i128)lam_pos * (i128)dP + ((i128)(lam_b * dB2) << 16);
+}
+
+template <bool PIXEL, bool GATED>
+__global__ void __launch_bounds__(PROP_THREADS) k_propose(const PhaseArgs a) {
+  if (sweep_skipped(a.prev)) return;
+  __shared__ int32_t tl[TY + 2][TX + 3];
+  const int lane = lane_id();
+  const int li = 2 * (threadIdx.x & 31) + a.cx;  // candidate block within the tile
+  const int lj = 2 * (threadIdx.x >> 5) + a.cy;
+  const int nbx = a.st.nbx, nby = a.st.nby;
+  const unsigned ntiles =
+      a.worklist ? *a.nwork : (unsigned)(a.st.tiles_x * a.st.tiles_y) * (unsigned)a.B;
+  unsigned c_cand = 0, c_topo = 0, c_prop = 0, c_srej = 0, c_commit = 0;
+
+  for (unsigned w = blockIdx.x; w < ntiles; w += gridDim.x) {
+    const unsigned t = a.worklist ? (unsigned)a.worklist[w] : w;
+    const int tx = (int)(t % (unsigned)a.st.tiles_x);
+    const unsigned rr0 = t / (unsigned)a.st.tiles_x;
+    const int ty = (int)(rr0 % (unsigned)a.st.tiles_y);
+    const int img = (int)(rr0 / (unsigned)a.st.tiles_y);
+    const int gx0 = tx * TX, gy0 = ty * TY;
+    int32_t *map = a.st.map + (size_t)img * nby * nbx;
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < (TY + 2) * (TX + 2); idx += PROP_THREADS) {
+      const int r = idx / (TX + 2), c = idx - r * (TX + 2);
+      const int gy = gy0 + r - 1, gx = gx0 + c - 1;
+      tl[r][c] = (gx >= 0 && gx < nbx && gy >= 0 && gy < nby) ? map[(size_t)gy * nbx + gx] : -1;
+    }
+    __syncthreads();
+
+    const int gx = gx0 + li, gy = gy0 + lj;
+    const bool valid = gx < nbx && gy < nby;
+    int A = -1;
+    int nq[4] = {-1, -1, -1, -1};
+    bool bnd = false;
+    if (valid) {
+      A = tl[lj + 1][li + 1];
+      nq[0] = tl[lj][li + 1];      // N
+      nq[1] = tl[lj + 1][li + 2];  // E
+      nq[2] = tl[lj + 2][li + 1];  // S
+      nq[3] = tl[lj + 1][li];      // W
+      bnd = (nq[0] >= 0 && nq[0] != A) | (nq[1] >= 0 && nq[1] != A) |
+            (nq[2] >= 0 && nq[2] != A) | (nq[3] >= 0 && nq[3] != A);
+    }
+    const int kb = img * a.M;
+    bool cand = false, topo = false, prop = false, srej = false;
+    int Bm = -1;
+    long long d[6] = {0, 0, 0, 0, 0, 0};
+    if (bnd) {
+      bool gate = true;
+      if (a.gating == 1) {
+        gate = a.sp.active[kb + A] != 0;
+      } else if (a.gating == 2) {  // Eq. 7 at block level
+        const int8_t yA = a.sp.y[kb + A];
+        gate = false;
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          if (nq[q] >= 0 && nq[q] != A && a.sp.y[kb + nq[q]] != yA) gate = true;
+      }
+      if (gate) {
+        cand = true;
+        unsigned m = 0;
+        m |= (unsigned)(tl[lj][li + 1] == A) << 0;
+        m |= (unsigned)(tl[lj][li + 2] == A) << 1;
+        m |= (unsigned)(tl[lj + 1][li + 2] == A) << 2;
+        m |= (unsigned)(tl[lj + 2][li + 2] == A) << 3;
+        m |= (unsigned)(tl[lj + 2][li + 1] == A) << 4;
+        m |= (unsigned)(tl[lj + 2][li] == A) << 5;
+        m |= (unsigned)(tl[lj + 1][li] == A) << 6;
+        m |= (unsigned)(tl[lj][li] == A) << 7;
+        if (simple_point(m)) {
+          topo = true;
+          long long e[4];
+          if (PIXEL) {
+            block_data_pix(a.image, a.H, a.W, img, gx, gy, d);
+            e[0] = e[1] = e[2] = e[3] = 1;
+          } else {
+            block_data_blk(a.st, img, gx, gy, d);
+            const long long bw = a.st.xs[gx + 1] - a.st.xs[gx], bh = a.st.ys[gy + 1] - a.st.ys[gy];
+            e[0] = bw; e[1] = bh; e[2] = bw; e[3] = bh;
+          }
+          const Rec recA = a.sp.rec[kb + A];
+          const RecV ra = rec_vals(recA);
+          bool have = false;
+          i128 bestE = 0;
+          int bestB = 0;
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const int B = nq[q];
+            bool skip = (B < 0) || (B == A);
+#pragma unroll
+            for (int r = 0; r < q; r++) skip |= (nq[r] == B);
+            if (skip) continue;
+            long long dB2 = 0;
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+              if (nq[r] >= 0) dB2 += e[r] * ((long long)(nq[r] != B) - (long long)(nq[r] != A));
+            const RecV rb = rec_vals(a.sp.rec[kb + B]);
+            const i128 E = delta_e(ra, rb, d, 2 * dB2, a.lam_pos, a.lam_b);
+            if (!have || E < bestE || (E == bestE && B < bestB)) {
+              have = true;
+              bestE = E;
+              bestB = B;
+            }
+          }
+          if (have && bestE < 0) {
+            if (a.size_mode != 0 &&
+                ((long long)recA.n - d[0]) * a.l_den < a.l_num * (long long)recA.init) {
+              srej = true;  // A12: the desired move would leave A below l * InitSize
+              if (a.size_mode == 2) {
+                a.sp.victim[kb + A] = 1;
+                *a.victim_any = 1u;
+              }
+            } else {
+              prop = true;
+              Bm = bestB;
+            }
+          }
+        }
+      }
+    }
+    c_cand += __popc(__ballot_sync(FULL, cand));
+    c_topo += __popc(__ballot_sync(FULL, topo));
+    c_srej += __popc(__ballot_sync(FULL, srej));
+    const unsigned pm = __ballot_sync(FULL, prop);
+    c_prop += __popc(pm);
+    if (pm) {
+      if (!GATED) {  // size_mode NONE: commit in place (no budget to check)
+        if (prop) map[(size_t)gy * nbx + gx] = Bm;
+        agg_sums(prop, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp, a.dlist, a.dcount);
+        agg_sums(prop, kb + Bm, d, false, a.sp.sums, a.sp.dirty, a.stamp, a.dlist, a.dcount);
+        c_commit += __popc(pm);
+      } else {
+        agg_add_i32(prop, kb + A, (int)d[0], a.sp.out);
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.prop_count, (unsigned long long)__popc(pm));
+        base = __shfl_sync(FULL, base, 0);
+        if (prop) {
+          const size_t idx = ((size_t)img * nby + gy) * nbx + gx;
+          a.props[base + __popc(pm & lanemask_lt())] =
+              (unsigned long long)idx | ((unsigned long long)(unsigned)Bm << 32);
+        }
+      }
+    }
+  }
+  if (lane == 0) {
+    if (c_cand) atomicAdd(&a.cnt[0], (unsigned long long)c_cand);
+    if (c_topo) atomicAdd(&a.cnt[1], (unsigned long long)c_topo);
+    if (c_prop) atomicAdd(&a.cnt[2], (unsigned long long)c_prop);
+    if (c_srej) atomicAdd(&a.cnt[3], (unsigned long long)c_srej);
+    if (c_commit) atomicAdd(&a.cnt[4], (unsigned long long)c_commit);
+  }
+}
+
+// ------------------------------------------------------------------ K5: commit
+template <bool PIXEL>
+__global__ void __launch_bounds__(256) k_commit(const PhaseArgs a) {
+  if (sweep_skipped(a.prev)) return;
+  const unsigned long long n = *a.prop_count;
+  const size_t nper = (size_t)a.st.nbx * a.st.nby;
+  unsigned c_commit = 0, c_rej = 0;
+  for (unsigned long long base = blockIdx.x * 256ull; base < n; base += gridDim.x * 256ull) {
+    const unsigned long long i = base + threadIdx.x;
+    const bool valid = i < n;
+    bool ok = false, rej = false;
+    int A = 0, B = 0, kb = 0;
+    long long d[6] = {0, 0, 0, 0, 0, 0};
+    size_t idx = 0;
+    if (valid) {
+      const unsigned long long pr = a.props[i];
+      idx = (size_t)(pr & 0xffffffffull);
+      B = (int)(pr >> 32);
+      const int img = (int)(idx / nper);
+      const size_t r = idx - (size_t)img * nper;
+      const int gy = (int)(r / a.st.nbx), gx = (int)(r - (size_t)gy * a.st.nbx);
+      kb = img * a.M;
+      A = a.st.map[idx];
+      const Rec ra = a.sp.rec[kb + A];
+      // O6' all-or-nothing budget: total proposed outflow must keep A >= l * InitSize (A19)
+      ok = !(((long long)ra.n - (long long)a.sp.out[kb + A]) * a.l_den < a.l_num * (long long)ra.init);
+      if (ok) {
+        if (PIXEL) block_data_pix(a.image, a.H, a.W, img, gx, gy, d);
+        else block_data_blk(a.st, img, gx, gy, d);
+        a.st.map[idx] = B;
+      } else {
+        rej = true;
+        if (a.size_mode == 2) {
+          a.sp.victim[kb + A] = 1;
+          *a.victim_any = 1u;
+        }
+      }
+    }
+    agg_sums(ok, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp, a.dlist, a.dcount);
+    agg_sums(ok, kb + B, d, false, a.sp.sums, a.sp.dirty, a.stamp, a.dlist, a.dcount);
+    c_commit += __popc(__ballot_sync(FULL, ok));
+    c_rej += __popc(__ballot_sync(FULL, rej));
+  }
+  if (lane_id() == 0) {
+    if (c_commit) atomicAdd(&a.cnt[4], (unsigned long long)c_commit);
+    if (c_rej) atomicAdd(&a.cnt[5], (unsigned long long)c_rej);
+  }
+}
+
+// ------------------------------------------------------- ordered compaction of u8 flags
+// chunk = 1024 flags per CTA of 256 threads (4 consecutive flags per thread)
+constexpr int CHUNK = 1024;
+
+__global__ void k_flag_count(const uint8_t *__restrict__ flags, int n, unsigned *chunk,
+                             const uint32_t *gate) {
+  if (gate && *gate == 0u) return;
+  __shared__ unsigned s;
+  if (threadIdx.x == 0) s = 0;
+  __syncthreads();
+  const int b0 = blockIdx.x * CHUNK + threadIdx.x * 4;
+  unsigned c = 0;
+#pragma unroll
+  for (int k = 0; k < 4; k++)
+    if (b0 + k < n) c += flags[b0 + k] != 0;
+  c = __reduce_add_sync(FULL, c);
+  if (lane_id() == 0) atomicAdd(&s, c);
+  __syncthreads();
+  if (threadIdx.x == 0) chunk[blockIdx.x] = s;
+}
+
+// single-CTA exclusive scan in place; *total = sum
+__global__ void k_scan_chunks(unsigned *chunk, int nchunks, unsigned *total, const uint32_t *gate) {
+  if (gate && *gate == 0u) return;
+  __shared__ unsigned warp_tot[32];
+  __shared__ unsigned carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nchunks; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    unsigned v = i < nchunks ? chunk[i] : 0u;
+    // inclusive warp scan
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned y = __shfl_up_sync(FULL, x, o);
+      if (lane_id() >= o) x += y;
+    }
+    if (lane_id() == 31) warp_tot[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int nw = blockDim.x >> 5;
+      unsigned t = threadIdx.x < nw ? warp_tot[threadIdx.x] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned y = __shfl_up_sync(FULL, t, o);
+        if (lane_id() >= o) t += y;
+      }
+      warp_tot[threadIdx.x] = t;  // inclusive
+    }
+    __syncthreads();
+    const unsigned woff = (threadIdx.x >> 5) ? warp_tot[(threadIdx.x >> 5) - 1] : 0u;
+    if (i < nchunks) chunk[i] = carry + woff + x - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_tot[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void k_flag_scatter(const uint8_t *__restrict__ flags, int n, const unsigned *chunk,
+                               int32_t *list, const uint32_t *gate) {
+  if (gate && *gate == 0u) return;
+  __shared__ unsigned warp_tot[8];
+  const int b0 = blockIdx.x * CHUNK + threadIdx.x * 4;
+  unsigned c = 0;
+  uint8_t f[4];
+#pragma unroll
+  for (int k = 0; k < 4; k++) {
+    f[k] = (b0 + k < n) ? flags[b0 + k] : 0;
+    c += f[k] != 0;
+  }
+  unsigned x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned y = __shfl_up_sync(FULL, x, o);
+    if (lane_id() >= o) x += y;
+  }
+  if (lane_id() == 31) warp_tot[threadIdx.x >> 5] = x;
+  __syncthreads();
+  unsigned woff = 0;
+  for (int w = 0; w < (int)(threadIdx.x >> 5); w++) woff += warp_tot[w];
+  unsigned pos = chunk[blockIdx.x] + woff + x - c;
+#pragma unroll
+  for (int k = 0; k < 4; k++)
+    if (f[k]) list[pos++] = b0 + k;
+}
+
+// ------------------------------------------------------------------ K6: merge round
+__device__ __forceinline__ unsigned long long hmix(unsigned long long k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
+constexpr unsigned long long HEMPTY = ~0ull;
+
+__device__ void hash_add(const MergeArgs &a, int V, int T, unsigned e) {
+  const unsigned long long key = ((unsigned long long)(unsigned)V << 32) | (unsigned)T;
+  unsigned long long h = hmix(key) & a.hmask;
+  while (true) {
+    const unsigned long long old = atomicCAS(&a.hkeys[h], HEMPTY, key);
+    if (old == HEMPTY) {
+      atomicAdd(&a.hvals[h], e);
+      a.hnext[h] = atomicExch(&a.head[V], (int)h);
+      return;
+    }
+    if (old == key) {
+      atomicAdd(&a.hvals[h], e);
+      return;
+    }
+    h = (h + 1) & a.hmask;
+  }
+}
+
+// victims: head[V] = -1
+__global__ void k_merge_heads(const MergeArgs a) {
+  if (*a.victim_any == 0u) return;
+  const unsigned nv = *a.total;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x)
+    a.head[a.vlist[i]] = -1;
+}
+
+// O7 step 1: (victim, neighbour) -> shared edge length over unordered 4-adjacent block pairs
+__global__ void k_merge_adjacency(const MergeArgs a) {
+  if (*a.victim_any == 0u) return;
+  const StageDev &st = a.st;
+  const size_t nper = (size_t)st.nbx * st.nby;
+  const size_t n = nper * a.B;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const int img = (int)(t / nper);
+    const size_t r = t - (size_t)img * nper;
+    const int gy = (int)(r / st.nbx), gx = (int)(r - (size_t)gy * st.nbx);
+    const int kb = img * a.M;
+    const int la = st.map[t];
+    const bool va = a.sp.victim[kb + la] != 0;
+    if (gx + 1 < st.nbx) {
+      const int lb = st.map[t + 1];
+      if (lb != la) {
+        const unsigned e = (unsigned)(st.ys[gy + 1] - st.ys[gy]);
+        if (va) hash_add(a, kb + la, kb + lb, e);
+        if (a.sp.victim[kb + lb]) hash_add(a, kb + lb, kb + la, e);
+      }
+    }
+    if (gy + 1 < st.nby) {
+      const int lb = st.map[t + st.nbx];
+      if (lb != la) {
+        const unsigned e = (unsigned)(st.xs[gx + 1] - st.xs[gx]);
+        if (va) hash_add(a, kb + la, kb + lb, e);
+        if (a.sp.victim[kb + lb]) hash_add(a, kb + lb, kb + la, e);
+      }
+    }
+  }
+}
+
+__global__ void k_merge_degree(const MergeArgs a) {
+  if (*a.victim_any == 0u) return;
+  const unsigned nv = *a.total;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x) {
+    unsigned c = 0;
+    for (int h = a.head[a.vlist[i]]; h >= 0; h = a.hnext[h]) c++;
+    a.deg[i] = c;
+  }
+}
+
+// exclusive scan of deg[0..nv) by a single CTA (victims per stage are few)
+__global__ void k_merge_scan_deg(const MergeArgs a) {
+  if (*a.victim_any == 0u) return;
+  __shared__ unsigned warp_tot[32];
+  __shared__ unsigned carry;
+  const int nv = (int)*a.total;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nv; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    unsigned v = i < nv ? a.deg[i] : 0u;
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned y = __shfl_up_sync(FULL, x, o);
+      if (lane_id() >= o) x += y;
+    }
+    if (lane_id() == 31) warp_tot[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int nw = blockDim.x >> 5;
+      unsigned t = threadIdx.x < nw ? warp_tot[threadIdx.x] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned y = __shfl_up_sync(FULL, t, o);
+        if (lane_id() >= o) t += y;
+      }
+      warp_tot[threadIdx.x] = t;
+    }
+    __syncthreads();
+    const unsigned woff = (threadIdx.x >> 5) ? warp_tot[(threadIdx.x >> 5) - 1] : 0u;
+    if (i < nv) a.deg[i] = carry + woff + x - v;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_tot[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    a.deg[nv] = carry;
+    *a.deg_total = carry;
+  }
+}
+
+__device__ __forceinline__ i128 merge_energy(const MergeArgs &a, int A, int T, long long len) {
+  // ΔE_m of relabelling all of A to T (A14): A's whole sums as the pixel set
+  const unsigned long long *s = a.sp.sums + (size_t)A * SUMW;
+  const RecV ra = rec_vals(a.sp.rec[A]), rt = rec_vals(a.sp.rec[T]);
+  const i128 n = (i128)(long long)s[0];
+  const long long cA[3] = {ra.c0, ra.c1, ra.c2}, cT[3] = {rt.c0, rt.c1, rt.c2};
+  i128 dC = 0, dP = 0;
+#pragma unroll
+  for (int ch = 0; ch < 3; ch++)
+    dC += (i128)(cT[ch] - cA[ch]) * (n * (i128)(cT[ch] + cA[ch]) - ((i128)(long long)s[1 + ch] << (FRAC + 1)));
+  dP += (i128)(rt.mx - ra.mx) * (n * (i128)(rt.mx + ra.mx) - ((i128)(long long)s[4] << (FRAC + 1)));
+  dP += (i128)(rt.my - ra.my) * (n * (i128)(rt.my + ra.my) - ((i128)(long long)s[5] << (FRAC + 1)));
+  return (dC << 16) + (i128)a.lam_pos * dP - ((i128)a.lam_b * (i128)(2 * len) << 16);
+}
+
+// candidates of every victim: Eq. 5-feasible neighbours sorted by (ΔE_m, T)
+__global__ void k_merge_fill(const MergeArgs a) {
+  if (*a.victim_any == 0u) return;
+  const unsigned nv = *a.total;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x) {
+    const int A = a.vlist[i];
+    const unsigned off = a.deg[i];
+    unsigned c = 0;
+    const long long nA = (long long)a.sp.sums[(size_t)A * SUMW];
+    for (int h = a.head[A]; h >= 0; h = a.hnext[h]) {
+      const int T = (int)(a.hkeys[h] & 0xffffffffull);
+      const long long nT = (long long)a.sp.sums[(size_t)T * SUMW];
+      // Eq. 5: Size(T) + Size(A) <= u * InitSize(T)
+      const bool feas = (nT + nA) * a.u_den <= a.u_num * (long long)a.sp.init[T];
+      const i128 E = merge_energy(a, A, T, (long long)a.hvals[h]);
+      // insertion into the sorted segment [off, off+c)
+      unsigned k = c;
+      while (k > 0) {
+        const unsigned p = off + k - 1;
+        const int Tp = a.candT[p];
+        const i128 Ep = (i128)((unsigned __int128)a.candE[2 * p] << 64 | a.candE[2 * p + 1]);
+        const bool later = feas ? (Tp < 0 || E < Ep || (E == Ep && T < Tp)) : false;
+        if (!later) break;
+        a.candT[p + 1] = Tp;
+        a.candE[2 * (p + 1)] = a.candE[2 * p];
+        a.candE[2 * (p + 1) + 1] = a.candE[2 * p + 1];
+        k--;
+      }
+      a.candT[off + k] = feas ? T : -1;
+      a.candE[2 * (off + k)] = (unsigned long long)((unsigned __int128)E >> 64);
+      a.candE[2 * (off + k) + 1] = (unsigned long long)E;
+      c++;
+    }
+  }
+}
+
+// O7 steps 3-4: victims in ascending id, first unlocked candidate wins; locks in smem bits
+__global__ void k_merge_sequential(const MergeArgs a, int use_smem) {
+  if (*a.victim_any == 0u) return;
+  extern __shared__ unsigned lockbits[];
+  const int nwords = (a.K + 31) / 32;
+  if (use_smem)
+    for (int w = threadIdx.x; w < nwords; w += blockDim.x) lockbits[w] = 0u;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  uint32_t *glock = reinterpret_cast<uint32_t *>(a.sp.out);  // reuse: out[] is free here
+  auto locked = [&](int k) -> bool {
+    return use_smem ? ((lockbits[k >> 5] >> (k & 31)) & 1u) : (glock[k] != 0u);
+  };
+  auto lock = [&](int k) {
+    if (use_smem) lockbits[k >> 5] |= 1u << (k & 31);
+    else glock[k] = 1u;
+  };
+  const unsigned nv = *a.total;
+  unsigned np = 0;
+  for (unsigned i = 0; i < nv; i++) {
+    const int A = a.vlist[i];
+    if (locked(A)) continue;
+    const unsigned e = a.deg[i + 1];
+    for (unsigned p = a.deg[i]; p < e; p++) {
+      const int T = a.candT[p];
+      if (T < 0) break;  // infeasible entries sort last
+      if (locked(T)) continue;
+      a.pairs[2 * np] = A;
+      a.pairs[2 * np + 1] = T;
+      np++;
+      lock(A);
+      lock(T);
+      break;
+    }
+  }
+  *a.npairs = np;
+  a.stage_info[0] += nv;
+  a.stage_info[1] += np;
+  if (np) *a.remap_pending = 1u;
+}
+
+__global__ void k_merge_apply(const MergeArgs a) {
+  if (*a.victim_any == 0u) return;
+  const unsigned np = *a.npairs;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+    const int A = a.pairs[2 * i], T = a.pairs[2 * i + 1];
+#pragma unroll
+    for (int f = 0; f < 6; f++) {
+      a.sp.sums[(size_t)T * SUMW + f] += a.sp.sums[(size_t)A * SUMW + f];
+      a.sp.sums[(size_t)A * SUMW + f] = 0ull;
+    }
+    a.sp.alive[A] = 0;
+    a.sp.active[A] = 0;
+    a.sp.y[A] = 0;
+    a.sp.remap[A] = T % a.M;  // local id of the target
+  }
+}
+
+__global__ void k_merge_cleanup(const MergeArgs a, int glock_clear) {
+  if (*a.victim_any == 0u) return;
+  const unsigned nv = *a.total;
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x) {
+    const int A = a.vlist[i];
+    a.sp.victim[A] = 0;
+    for (int h = a.head[A]; h >= 0; h = a.hnext[h]) {
+      if (glock_clear) {
+        const int T = (int)(a.hkeys[h] & 0xffffffffull);
+        reinterpret_cast<uint32_t *>(a.sp.out)[T] = 0u;
+      }
+      a.hkeys[h] = HEMPTY;
+      a.hvals[h] = 0u;
+    }
+    if (glock_clear) reinterpret_cast<uint32_t *>(a.sp.out)[A] = 0u;
+  }
+}
+
+__global__ void k_merge_done(const MergeArgs a) { *a.victim_any = 0u; }
+
+// ------------------------------------------------------------------ K7: prediction
+__global__ void k_predict_y(const PredictArgs a) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.K; k += gridDim.x * blockDim.x) {
+    if (!a.sp.alive[k]) {
+      a.sp.y[k] = 0;
+      a.sp.active[k] = 0;
+      continue;
+    }
+    const Rec r = a.sp.rec[k];
+    const long long c[3] = {(long long)(r.cq01 & 0xffffu), (long long)(r.cq01 >> 16),
+                            (long long)(r.cq2f & 0xffffu)};
+    long long dmin = -1;
+    for (int t = 0; t < a.n_proto; t++) {
+      long long dd = 0;
+#pragma unroll
+      for (int ch = 0; ch < 3; ch++) {
+        const long long e = c[ch] - ((long long)a.proto[t][ch] << FRAC);
+        dd += e * e;
+      }
+      if (dmin < 0 || dd < dmin) dmin = dd;
+    }
+    const int8_t y = ((a.tau2 << (2 * FRAC)) - dmin >= 0) ? 1 : -1;  // Eq. 6
+    a.sp.y[k] = y;
+    a.sp.active[k] = (a.mask_rule == 1) ? (y == 1) : 0;
+  }
+}
+
+__device__ __forceinline__ int resolve(const SpDev &sp, int kb, int l, bool remap) {
+  if (remap && !sp.alive[kb + l]) return sp.remap[kb + l];
+  return l;
+}
+
+// boundary superpixels: a 4-adjacent superpixel of the other class
+__global__ void k_predict_bsp(const PredictArgs a) {
+  const StageDev &st = a.st;
+  const bool rm = *a.remap_pending != 0u;
+  const size_t nper = (size_t)st.nbx * st.nby;
+  const size_t n = nper * a.B;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const int img = (int)(t / nper);
+    const size_t r = t - (size_t)img * nper;
+    const int gy = (int)(r / st.nbx), gx = (int)(r - (size_t)gy * st.nbx);
+    const int kb = img * a.M;
+    const int la = resolve(a.sp, kb, st.map[t], rm);
+    if (gx + 1 < st.nbx) {
+      const int lb = resolve(a.sp, kb, st.map[t + 1], rm);
+      if (la != lb && a.sp.y[kb + la] != a.sp.y[kb + lb]) {
+        a.sp.active[kb + la] = 1;
+        a.sp.active[kb + lb] = 1;
+      }
+    }
+    if (gy + 1 < st.nby) {
+      const int lb = resolve(a.sp, kb, st.map[t + st.nbx], rm);
+      if (la != lb && a.sp.y[kb + la] != a.sp.y[kb + lb]) {
+        a.sp.active[kb + la] = 1;
+        a.sp.active[kb + lb] = 1;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K8: transition
+__global__ void __launch_bounds__(256) k_transition(const TransArgs a) {
+  const StageDev &pv = a.prev, &nx = a.next;
+  const unsigned t = blockIdx.x;
+  const int tx = (int)(t % (unsigned)nx.tiles_x);
+  const unsigned rr = t / (unsigned)nx.tiles_x;
+  const int ty = (int)(rr % (unsigned)nx.tiles_y);
+  const int img = (int)(rr / (unsigned)nx.tiles_y);
+  const int kb = img * a.M;
+  const bool rm = *a.remap_pending != 0u;
+  const int32_t *pmap = pv.map + (size_t)img * pv.nby * pv.nbx;
+  int32_t *nmap = nx.map + (size_t)img * nx.nby * nx.nbx;
+  int act = 0;
+  int last = -1;
+  for (int k = threadIdx.x; k < TX * TY; k += 256) {
+    const int gx = tx * TX + (k % TX), gy = ty * TY + (k / TX);
+    int l = -1;
+    if (gx < nx.nbx && gy < nx.nby) {
+      l = pmap[(size_t)nx.py[gy] * pv.nbx + nx.px[gx]];
+      if (rm && !a.sp.alive[kb + l]) l = a.sp.remap[kb + l];
+      nmap[(size_t)gy * nx.nbx + gx] = l;
+      if (a.gate && l != last) {
+        act |= a.sp.active[kb + l];
+        last = l;
+      }
+    }
+  }
+  if (a.gate) {
+    act = __syncthreads_or(act);
+    if (threadIdx.x == 0 && act) {
+      const unsigned p = atomicAdd(a.nwork, 1u);
+      a.worklist[p] = (int)t;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ RECOUNT
+template <bool PIXEL>
+__global__ void k_recount(const RecountArgs a) {
+  const StageDev &st = a.st;
+  const size_t nper = (size_t)st.nbx * st.nby;
+  const size_t n = nper * a.B;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t base = blockIdx.x * (size_t)blockDim.x; base < n; base += stride) {
+    const size_t t = base + threadIdx.x;
+    const bool valid = t < n;
+    long long d[6] = {0, 0, 0, 0, 0, 0};
+    int key = 0;
+    if (valid) {
+      const int img = (int)(t / nper);
+      const size_t r = t - (size_t)img * nper;
+      const int gy = (int)(r / st.nbx), gx = (int)(r - (size_t)gy * st.nbx);
+      if (PIXEL) block_data_pix(a.image, a.H, a.W, img, gx, gy, d);
+      else block_data_blk(st, img, gx, gy, d);
+      key = img * a.M + st.map[t];
+    }
+    agg_sums(valid, key, d, false, a.rc, nullptr, 0, nullptr, nullptr);
+  }
+}
+
+__global__ void k_recount_check(const RecountArgs a) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.K; k += gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int f = 0; f < 6; f++) {
+      if (a.rc[(size_t)k * SUMW + f] != a.sp.sums[(size_t)k * SUMW + f]) *a.err = 1u;
+      a.rc[(size_t)k * SUMW + f] = 0ull;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K9: final
+__global__ void k_final_upsample(const FinalArgs a) {
+  const bool rm = *a.remap_pending != 0u;
+  const size_t nper = (size_t)a.H * a.W;
+  const size_t n = nper * a.B;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const int img = (int)(t / nper);
+    const size_t r = t - (size_t)img * nper;
+    const int y = (int)(r / a.W), x = (int)(r - (size_t)y * a.W);
+    int l = a.last.map[((size_t)img * a.last.nby + a.byp[y]) * a.last.nbx + a.bxp[x]];
+    if (rm && !a.sp.alive[img * a.M + l]) l = a.sp.remap[img * a.M + l];
+    a.labels[t] = l;
+  }
+}
+
+__global__ void k_final_remap(const FinalArgs a) {
+  if (*a.remap_pending == 0u) return;
+  const size_t nper = (size_t)a.H * a.W;
+  const size_t n = nper * a.B;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const int img = (int)(t / nper);
+    const int l = a.labels[t];
+    if (!a.sp.alive[img * a.M + l]) a.labels[t] = a.sp.remap[img * a.M + l];
+  }
+}
+
+// =================================================================== launch wrappers
+static int grid_for(size_t n, int threads, int cap = 148 * 16) {
+  size_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > (size_t)cap) g = cap;
+  return (int)g;
+}
+
+void launch_init_sp(const InitArgs &a, cudaStream_t s) {
+  k_init_sp<<<grid_for(a.K, 256), 256, 0, s>>>(a);
+}
+
+void launch_pyramid_leaf(const StageDev &st, const uint8_t *image, int H, int W, int B,
+                         uint64_t *bsum, cudaStream_t s) {
+  const size_t n = (size_t)st.nbx * st.nby * B;
+  k_pyramid_leaf<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(st, image, H, W, B, bsum);
+}
+
+void launch_pyramid_up(const StageDev &parent, const StageDev &child, int B, uint64_t *bsum,
+                       cudaStream_t s) {
+  const size_t n = (size_t)parent.nbx * parent.nby * B;
+  k_pyramid_up<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(parent, child, B, bsum);
+}
+
+void launch_init_map0(const InitArgs &a, cudaStream_t s) {
+  const size_t n = (size_t)a.st0.nbx * a.st0.nby * a.B;
+  k_init_map0<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(a);
+}
+
+void launch_stats0(const InitArgs &a, cudaStream_t s) {
+  const size_t n = (size_t)a.st0.nbx * a.st0.nby * a.B;
+  if (a.st0.b == 1) k_stats0<true><<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(a);
+  else k_stats0<false><<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(a);
+}
+
+void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s) {
+  k_snapshot<<<grid, 256, 0, s>>>(a);
+}
+
+int propose_occupancy(bool pixel, bool gated) {
+  int nb = 0;
+  if (pixel && gated) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propose<true, true>, PROP_THREADS, 0);
+  if (pixel && !gated) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propose<true, false>, PROP_THREADS, 0);
+  if (!pixel && gated) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propose<false, true>, PROP_THREADS, 0);
+  if (!pixel && !gated) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propose<false, false>, PROP_THREADS, 0);
+  return nb < 1 ? 1 : nb;
+}
+
+void launch_propose(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
+  const bool gated = a.size_mode != 0;
+  if (pixel && gated) k_propose<true, true><<<grid, PROP_THREADS, 0, s>>>(a);
+  else if (pixel) k_propose<true, false><<<grid, PROP_THREADS, 0, s>>>(a);
+  else if (gated) k_propose<false, true><<<grid, PROP_THREADS, 0, s>>>(a);
+  else k_propose<false, false><<<grid, PROP_THREADS, 0, s>>>(a);
+}
+
+void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
+  if (pixel) k_commit<true><<<grid, 256, 0, s>>>(a);
+  else k_commit<false><<<grid, 256, 0, s>>>(a);
+}
+
+void launch_merge_round(const MergeArgs &a, int grid, cudaStream_t s, int *nlaunch) {
+  const int nchunks = (a.K + CHUNK - 1) / CHUNK;
+  k_flag_count<<<nchunks, 256, 0, s>>>(a.sp.victim, a.K, a.chunk, a.victim_any);
+  k_scan_chunks<<<1, 1024, 0, s>>>(a.chunk, nchunks, a.total, a.victim_any);
+  k_flag_scatter<<<nchunks, 256, 0, s>>>(a.sp.victim, a.K, a.chunk, a.vlist, a.victim_any);
+  k_merge_heads<<<grid, 256, 0, s>>>(a);
+  const size_t nb = (size_t)a.st.nbx * a.st.nby * a.B;
+  k_merge_adjacency<<<grid_for(nb, 256, 148 * 32), 256, 0, s>>>(a);
+  k_merge_degree<<<grid, 256, 0, s>>>(a);
+  k_merge_scan_deg<<<1, 1024, 0, s>>>(a);
+  k_merge_fill<<<grid, 256, 0, s>>>(a);
+  const size_t lock_bytes = (size_t)((a.K + 31) / 32) * 4;
+  const int use_smem = lock_bytes <= 200 * 1024;
+  if (use_smem && lock_bytes > 48 * 1024)
+    cudaFuncSetAttribute(k_merge_sequential, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lock_bytes);
+  k_merge_sequential<<<1, 256, use_smem ? lock_bytes : 0, s>>>(a, use_smem);
+  k_merge_apply<<<grid, 256, 0, s>>>(a);
+  k_merge_cleanup<<<grid, 256, 0, s>>>(a, use_smem ? 0 : 1);
+  k_merge_done<<<1, 1, 0, s>>>(a);
+  *nlaunch += 12;
+}
+
+void launch_predict(const PredictArgs &a, int grid, cudaStream_t s, int *nlaunch) {
+  k_predict_y<<<grid_for(a.K, 256), 256, 0, s>>>(a);
+  *nlaunch += 1;
+  if (a.mask_rule != 1) {
+    const size_t nb = (size_t)a.st.nbx * a.st.nby * a.B;
+    k_predict_bsp<<<grid_for(nb, 256, 148 * 32), 256, 0, s>>>(a);
+    *nlaunch += 1;
+  }
+  const int nchunks = (a.K + CHUNK - 1) / CHUNK;
+  k_flag_count<<<nchunks, 256, 0, s>>>(a.sp.active, a.K, a.chunk, nullptr);
+  k_scan_chunks<<<1, 1024, 0, s>>>(a.chunk, nchunks, a.total, nullptr);
+  k_flag_scatter<<<nchunks, 256, 0, s>>>(a.sp.active, a.K, a.chunk, a.alist, nullptr);
+  *nlaunch += 3;
+}
+
+void launch_transition(const TransArgs &a, cudaStream_t s) {
+  const unsigned ntiles = (unsigned)(a.next.tiles_x * a.next.tiles_y) * (unsigned)a.B;
+  k_transition<<<ntiles, 256, 0, s>>>(a);
+}
+
+void launch_recount(const RecountArgs &a, bool pixel, int grid, cudaStream_t s, int *nlaunch) {
+  const size_t n = (size_t)a.st.nbx * a.st.nby * a.B;
+  if (pixel) k_recount<true><<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(a);
+  else k_recount<false><<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(a);
+  k_recount_check<<<grid_for(a.K, 256), 256, 0, s>>>(a);
+  *nlaunch += 2;
+  (void)grid;
+}
+
+void launch_final(const FinalArgs &a, bool upsample, cudaStream_t s) {
+  const size_t n = (size_t)a.H * a.W * a.B;
+  if (upsample) k_final_upsample<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(a);
+  else k_final_remap<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(a);
+}
+
+}  // namespace rapid

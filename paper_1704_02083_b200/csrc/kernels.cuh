@@ -1,0 +1,134 @@
+// kernels.cuh — argument blocks and launch wrappers of the RAPID sm_100a kernels.
+#pragma once
+#include "common.cuh"
+
+namespace rapid {
+
+// ---- K4 / K5: one parity phase (propose, commit) --------------------------------------
+struct PhaseArgs {
+  StageDev st;
+  SpDev sp;
+  const uint8_t *image;
+  int32_t H, W, B, M;
+  int32_t cx, cy;            // phase colour (A5)
+  int32_t gating;            // 0 off, 1 active[A] (CLASS/BSP), 2 Eq. 7 (EQ7)
+  int32_t size_mode;         // RAPID_SIZE_*
+  long long l_num, l_den;
+  long long lam_pos, lam_b;  // Q16
+  const int32_t *worklist;   // null: every tile of the stage
+  const unsigned int *nwork; // device count of the worklist
+  unsigned long long *props; // proposals: stage-map index | B << 32
+  unsigned long long *prop_count;
+  int32_t *dlist;            // dirty list of this phase
+  unsigned int *dcount;
+  uint32_t stamp;
+  unsigned long long *cnt;        // [NCNT] counters of this phase
+  const unsigned long long *prev; // counters of the previous sweep (phase 0), or null
+  uint32_t *victim_any;
+};
+
+struct SnapArgs {
+  SpDev sp;
+  int32_t K;
+  const int32_t *list;        // dirty list (null: all K)
+  const unsigned int *count;
+};
+
+struct MergeArgs {
+  StageDev st;
+  SpDev sp;
+  int32_t B, M, K;
+  long long lam_pos, lam_b;
+  long long u_num, u_den;
+  uint32_t *victim_any;      // this stage's flag
+  uint32_t *remap_pending;   // this stage's flag (out)
+  // compaction scratch
+  unsigned int *chunk;       // per-chunk counts -> offsets
+  unsigned int *total;       // number of victims
+  int32_t *vlist;            // ordered victims
+  // adjacency hash
+  unsigned long long *hkeys;
+  unsigned int *hvals;
+  int32_t *hnext;
+  int32_t *head;             // [K]
+  unsigned long long hmask;
+  // candidates
+  unsigned int *deg;         // [victims] -> offsets (in place scan)
+  unsigned int *deg_total;
+  int32_t *candT;
+  unsigned long long *candE; // int128 as (hi, lo) pairs, bias-encoded for unsigned compare
+  int32_t *pairs;            // merges (A, T)
+  unsigned int *npairs;
+  unsigned long long *stage_info; // [4]: victims, merges, active tiles, -
+};
+
+struct PredictArgs {
+  StageDev st;
+  SpDev sp;
+  int32_t B, M, K;
+  int32_t mask_rule, n_proto;
+  int32_t proto[4][3];
+  long long tau2;
+  const uint32_t *remap_pending;
+  unsigned int *chunk;
+  unsigned int *total;
+  int32_t *alist;
+};
+
+struct TransArgs {
+  StageDev prev, next;
+  SpDev sp;
+  int32_t B, M;
+  const uint32_t *remap_pending;
+  int32_t gate;              // 1: build the active-tile worklist of `next`
+  int32_t *worklist;
+  unsigned int *nwork;
+};
+
+struct InitArgs {
+  StageDev st0;              // stage 0 (map, geometry, packed sums)
+  SpDev sp;
+  const uint8_t *image;
+  int32_t H, W, B, M, K;
+  int32_t rows, cols;
+  const int32_t *X, *Y;      // cell boundaries (cols+1, rows+1)
+  const int32_t *cellx, *celly; // cell index of each stage-0 block column / row
+};
+
+struct RecountArgs {
+  StageDev st;
+  SpDev sp;
+  const uint8_t *image;
+  int32_t H, W, B, M, K;
+  unsigned long long *rc;    // [K][SUMW] recount scratch (zeroed)
+  uint32_t *err;
+};
+
+struct FinalArgs {
+  StageDev last;
+  SpDev sp;
+  int32_t B, H, W, M;
+  const int32_t *bxp, *byp;  // block column / row of each pixel column / row
+  const uint32_t *remap_pending;
+  int32_t *labels;           // [B][H][W]
+};
+
+// launch wrappers (all enqueue on `s`)
+void launch_init_sp(const InitArgs &a, cudaStream_t s);
+void launch_pyramid_leaf(const StageDev &st, const uint8_t *image, int H, int W, int B,
+                         uint64_t *bsum, cudaStream_t s);
+void launch_pyramid_up(const StageDev &parent, const StageDev &child, int B, uint64_t *bsum,
+                       cudaStream_t s);
+void launch_init_map0(const InitArgs &a, cudaStream_t s);
+void launch_stats0(const InitArgs &a, cudaStream_t s);
+void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s);
+void launch_propose(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
+void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
+void launch_merge_round(const MergeArgs &a, int grid, cudaStream_t s, int *nlaunch);
+void launch_predict(const PredictArgs &a, int grid, cudaStream_t s, int *nlaunch);
+void launch_transition(const TransArgs &a, cudaStream_t s);
+void launch_recount(const RecountArgs &a, bool pixel, int grid, cudaStream_t s, int *nlaunch);
+void launch_final(const FinalArgs &a, bool upsample, cudaStream_t s);
+int propose_occupancy(bool pixel, bool gated);
+
+}  // namespace rapid

@@ -1,0 +1,181 @@
+"""GPU parity: the sm_100a path (called through the C ABI) against the CPU oracle, element
+by element, on seeded synthetic inputs.  Bar: bit-exact labels, exact int64 sums, identical
+flags and per-phase move counts; derived float means within 1e-6 relative."""
+import copy
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import assert_parity, gpu_run
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rapid():
+    import torch
+    import paper_1704_02083_b200 as rb
+    assert torch.cuda.is_available()
+    r = rb.Rapid(0, max_pixels=1 << 27, max_superpixels=1 << 17)
+    yield r
+    r.close()
+
+
+def P(M, sizes, sweeps=3, lam_pos=65536, lam_b=32 * 65536, size_mode=0, mask=0, l=(1, 4),
+      u=(3, 2), tau2=1600, stats=0):
+    return synth.Params(M, list(sizes), sweeps, lam_pos, lam_b, size_mode, l[0], l[1], u[0], u[1],
+                        mask, [synth.PROTO_PINK, synth.PROTO_PURPLE], tau2, stats)
+
+
+# ----------------------------------------------------------------------- hand-worked H1
+def test_H1_on_gpu(rapid):
+    img = np.zeros((8, 8, 3), dtype=np.uint8)
+    img[:, 3:, :] = 200
+    o, lab, sp, info = assert_parity(rapid, img, P(2, [2, 1], 2))
+    want = np.zeros((8, 8), dtype=np.int32)
+    want[:, 3:] = 1
+    assert np.array_equal(lab[0], want)
+    assert info.counters()[1, 0, :, oracle.C_COMMIT].tolist() == [0, 4, 0, 4]
+
+
+# ----------------------------------------------------------------------- full configs
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_config1_full(rapid, mode):
+    w = synth.config(1)
+    p = copy.deepcopy(w.params)
+    p.size_mode = mode
+    assert_parity(rapid, w.images(), p)
+
+
+def test_config1_recount_equals_reuse(rapid):
+    w = synth.config(1)
+    p = copy.deepcopy(w.params)
+    p.stats_mode = synth.STATS_RECOUNT
+    o, lab, sp, info = assert_parity(rapid, w.images(), p)
+    assert info.status == 0
+
+
+def test_config2_full(rapid):
+    w = synth.config(2)
+    assert_parity(rapid, w.images(), w.params)
+
+
+@pytest.mark.slow
+def test_config3_full(rapid):
+    w = synth.config(3)
+    o, lab, sp, info = assert_parity(rapid, w.images(), w.params)
+    assert 0 < info.active < info.alive
+
+
+@pytest.mark.slow
+def test_config5_batch_full(rapid):
+    w = synth.config(5)
+    assert_parity(rapid, w.images(), w.params)
+
+
+def test_config4_scaled_sample(rapid):
+    """config 4's densities, prediction mask and merges at 2048^2 (full pipeline)."""
+    w = synth.scaled(4, 2048, 2048)
+    assert_parity(rapid, w.images(), w.params)
+
+
+# ----------------------------------------------------------------------- random cases
+def _cases(seed, n):
+    rng = np.random.default_rng(seed)
+    for _ in range(n):
+        H, W = int(rng.integers(17, 150)), int(rng.integers(17, 150))
+        M = int(rng.integers(2, max(3, H * W // 150)))
+        try:
+            oracle.grid(H, W, M)
+        except oracle.OracleError:
+            continue
+        regions = int(rng.integers(2, 12))
+        img = synth.image(H, W, int(rng.integers(1 << 30)), regions, int(rng.integers(0, 30)),
+                          int(rng.integers(0, 400)))
+        sizes = [[8, 4, 2, 1], [16, 8, 4, 2, 1], [4, 2, 1], [4, 1], [2], [8, 4], [32, 16, 8, 4, 2, 1]][
+            int(rng.integers(7))]
+        yield rng, img, M, sizes
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_random_small_all_size_modes(rapid, mode):
+    for rng, img, M, sizes in _cases(100 + mode, 12):
+        p = P(M, sizes, int(rng.integers(1, 5)), int(rng.integers(0, 6 * 65536)),
+              int(rng.integers(0, 64 * 65536)), size_mode=mode)
+        assert_parity(rapid, img, p)
+
+
+@pytest.mark.parametrize("mask", [1, 2, 3])
+def test_random_small_mask_rules(rapid, mask):
+    for rng, img, M, sizes in _cases(200 + mask, 10):
+        p = P(M, sizes, 3, size_mode=int(rng.integers(0, 3)), mask=mask,
+              tau2=int(rng.integers(200, 6000)))
+        assert_parity(rapid, img, p)
+
+
+def test_random_batches(rapid):
+    rng = np.random.default_rng(7)
+    for _ in range(4):
+        B = int(rng.integers(2, 6))
+        H, W = int(rng.integers(40, 120)), int(rng.integers(40, 120))
+        imgs = np.stack([synth.image(H, W, int(rng.integers(1 << 30)), 6, 20, 200) for _ in range(B)])
+        p = P(12, [8, 4, 2, 1], 3, size_mode=2, mask=int(rng.integers(0, 4)))
+        o, lab, sp, info = assert_parity(rapid, imgs, p)
+        for b in range(B):  # batch == singles
+            l1, sp1, _ = gpu_run(rapid, imgs[b], p)
+            assert np.array_equal(l1[0], lab[b])
+
+
+# ----------------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("H,W,M,sizes", [
+    (1, 1, 1, [1]),
+    (1, 40, 4, [4, 2, 1]),
+    (37, 1, 3, [2, 1]),
+    (5, 7, 35, [4, 2, 1]),        # every pixel its own superpixel
+    (64, 64, 1, [32, 16, 1]),     # M = 1: nothing moves
+    (130, 70, 9, [64, 32, 16, 8, 4, 2, 1]),  # maximum block size
+    (33, 65, 6, [8, 4]),          # final grain 4 with ragged borders
+])
+def test_edge_shapes(rapid, H, W, M, sizes):
+    img = synth.image(H, W, 11, 3, 2, 0)
+    for mode in (0, 2):
+        assert_parity(rapid, img, P(M, sizes, 3, size_mode=mode))
+
+
+def test_zero_sweeps_and_constant_image(rapid):
+    img = synth.image(96, 80, 5, 5, 10, 0)
+    assert_parity(rapid, img, P(20, [8, 4, 2, 1], 0))
+    const = np.full((64, 96, 3), 77, dtype=np.uint8)
+    o, lab, sp, info = assert_parity(rapid, const, P(24, [8, 4, 2, 1], 3, size_mode=2))
+    assert info.counters()[..., oracle.C_COMMIT].sum() == 0
+
+
+def test_determinism_and_host_api(rapid):
+    w = synth.config(2)
+    img = w.images()
+    l1, s1, _ = gpu_run(rapid, img, w.params)
+    l2, s2, _ = gpu_run(rapid, img, w.params)
+    assert np.array_equal(l1, l2) and np.array_equal(s1, s2)
+    lh = rapid.segment_host(img, w.params)
+    assert np.array_equal(lh, l1)
+
+
+def test_debug_stop_points_match_oracle(rapid):
+    import torch
+    w = synth.config(1)
+    img = w.images()
+    p = copy.deepcopy(w.params)
+    p.size_mode = 2
+    t = torch.from_numpy(img).cuda()
+    cap = (w.H + 2) * (w.W + 2) * 2
+    for pt in [(oracle.STOP_STAGE_START, 2, 0, 0), (oracle.STOP_PHASE, 3, 1, 2),
+               (oracle.STOP_AFTER_MERGE, 3, 0, 0), (oracle.STOP_PHASE, 4, 0, 3)]:
+        o = oracle.segment(img, p, stop=pt, map_cap=cap)
+        rapid.debug_stop(*pt)
+        rapid.segment(t, p)
+        torch.cuda.synchronize()
+        g = rapid.debug_map(cap)
+        rapid.debug_stop(0)
+        assert np.array_equal(g, o.map), pt

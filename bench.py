@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""Benchmark: Mpixel/s per full RAPID segmentation on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+A step is one full segmentation (rapid_segment: pyramid, every stage's parity sweeps,
+merges, prediction, transitions, final) of the workload's synthetic input, already resident
+in HBM.  Default workload: BASELINE.json configs[3] (config 4: 32768x32768, 1 Gpx, M=2^20,
+full RAPID pipeline) — the 1-Gpixel configuration the north star's roofline target names.
+Inputs are larger than L2 (3.2 GB image, 4.3 GB label map), so no L2 flush is needed.
+
+N>1 (torchrun): every rank segments its own image (different seed): weak scaling, no
+collective on the data path ("replicas only").  Timing: W untimed warm-up
+steps, then K steps bracketed by barrier + cuda.synchronize, CUDA events on the stream,
+max over ranks.  --impl reference times the CPU oracle (the reference arm of this tier) on
+a bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+METRIC = "Mpixel/s per full segmentation at 1 B200; HBM GB/s fraction of peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sample", type=int, default=2048, help="side of the bounded CPU sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_for_rank(cfg, rank):
+    w = synth.config(cfg)
+    if rank:
+        w.seeds = [s + 1000 * rank for s in w.seeds]
+    return w
+
+
+def peaks():
+    try:
+        with open(MEASURED) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def config_dict(w, extra=None):
+    p = w.params
+    d = {"workload": w.name, "batch": w.B, "H": w.H, "W": w.W, "superpixels_per_image": p.n_superpixels,
+         "block_sizes": p.block_sizes, "sweeps": p.sweeps,
+         "size_mode": ["NONE", "HARD", "MERGE"][p.size_mode],
+         "mask_rule": ["OFF", "CLASS", "BSP", "EQ7"][p.mask_rule],
+         "stats_mode": ["REUSE", "RECOUNT"][p.stats_mode],
+         "l2": "inputs larger than L2 (image %.2f GB, labels %.2f GB); no flush" % (
+             w.pixels * 3 / 1e9, w.pixels * 4 / 1e9)}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_sample(cfg, side, seed_offset=0):
+    import oracle
+    sw = synth.scaled(cfg, side, side, seed_offset=seed_offset)
+    img = sw.images()
+    t0 = time.perf_counter()
+    oracle.segment(img, sw.params)
+    dt = time.perf_counter() - t0
+    return sw, dt
+
+
+def cpu_baseline(cfg, side):
+    sw, dt = oracle_sample(cfg, side)
+    return {"value": round(sw.pixels / dt / 1e6, 4), "unit": "Mpixel/s", "cores": 1, "kind": "oracle",
+            "sample": f"{sw.name}: {side}x{side} px with config {cfg}'s densities and parameters, "
+                      f"full pipeline, single-threaded C oracle, {dt:.2f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    w = synth.config(args.config)
+    times = []
+    for i in range(args.warmup + args.steps):
+        sw, dt = oracle_sample(args.config, args.sample, seed_offset=0)
+        if i >= args.warmup:
+            times.append(dt)
+    px = sw.pixels
+    tot = sum(times)
+    value = px * len(times) / tot / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Mpixel/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(tot / len(times) * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": config_dict(w, {"reference_sample": f"{args.sample}x{args.sample} per step"}),
+            "cpu_baseline": {"value": round(value, 4), "unit": "Mpixel/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{args.sample}x{args.sample} px of config {args.config}'s "
+                                       "workload (same densities/params) per step, single-threaded C oracle"},
+            "e2e": {"value": round(value, 4), "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    def __init__(self, index):
+        self.path = tempfile.mktemp(suffix=".csv")
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in open(self.path):
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- algorithmic bytes
+def phase_bytes(info, w, window):
+    """SURVEY §8(d) model per K4 launch: 4 B x window blocks + c_s x candidates needing colour
+    + 4 B x committed moves.  window[s] = blocks within Chebyshev distance 1 of a block whose
+    label can pass the gate (all blocks before prediction)."""
+    import paper_1704_02083_b200 as rb
+    cnt = info.counters()
+    out = {}
+    for s, b in enumerate(w.params.block_sizes):
+        cs = 3 if b == 1 else 8
+        run = int(info.stage_sweeps_run[s])
+        byt = 0
+        for t in range(run):
+            for ph in range(4):
+                byt += 4 * window[s] + cs * int(cnt[s, t, ph, rb.C_TOPO]) + 4 * int(cnt[s, t, ph, rb.C_COMMIT])
+        out[s] = (byt, run * 4)
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1704_02083_b200 as rb
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    w = workload_for_rank(args.config, rank)
+    p = w.params
+    t0 = time.time()
+    host = torch.empty((w.B, w.H, w.W, 3), dtype=torch.uint8).pin_memory()
+    w.images(out=host.numpy())
+    gen_s = time.time() - t0
+    img = host.to(dev)
+    labels = torch.empty((w.B, w.H, w.W), dtype=torch.int32, device=dev)
+    r = rb.Rapid(local, max_pixels=w.pixels, max_superpixels=w.B * p.n_superpixels)
+    stream = torch.cuda.current_stream(dev)
+
+    # untimed: one run with window counting for the algorithmic-bytes model
+    r.set_profiling(2)
+    r.segment(img, p, labels)
+    _, info = r.stats(0)
+    window = [int(info.stage_window_blocks[s]) for s in range(len(p.block_sizes))]
+    for _ in range(args.warmup):
+        r.segment(img, p, labels)
+    torch.cuda.synchronize()
+
+    # timed region: K segmentations, events on the launching stream; profiling events on
+    r.set_profiling(1)
+    clocks = Clocks(local) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prof_ms = np.zeros((rb.NK, rb.MAX_STAGES))
+    prof_launch = np.zeros((rb.NK, rb.MAX_STAGES))
+    total_launches = 0
+    ev0.record(stream)
+    for _ in range(args.steps):
+        r.segment(img, p, labels)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    dev_ms = ev0.elapsed_time(ev1)
+    ck = clocks.stop() if clocks else None
+    # per-kernel profile of the timed steps (profile() reports the last segmentation)
+    pr = r.profile()
+    prof_ms += pr.ms_array()
+    prof_launch += pr.launch_array()
+    total_launches = int(pr.total_launches)
+    _, info = r.stats(0)
+
+    t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    px_total = w.pixels * world * args.steps
+    value = px_total / (ms_max / 1e3) / 1e6
+
+    # end to end through the public host API: H2D image + D2H labels every step
+    e2e = None
+    if not args.no_e2e:
+        r.set_profiling(0)
+        hl = torch.empty((w.B, w.H, w.W), dtype=torch.int32).pin_memory()
+        hn, ln = host.numpy(), hl.numpy()
+        r.segment_host(hn, p, ln)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = time.perf_counter()
+        ee0 = torch.cuda.Event(enable_timing=True)
+        ee1 = torch.cuda.Event(enable_timing=True)
+        ee0.record(stream)
+        for _ in range(args.steps):
+            r.segment_host(hn, p, ln)
+        ee1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = ee0.elapsed_time(ee1)
+        wall = (time.perf_counter() - e0) * 1e3
+        te = torch.tensor([max(e_ms, wall)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(w.pixels * world * args.steps / (float(te.item()) / 1e3) / 1e6, 3),
+               "unit": "Mpixel/s", "h2d_bytes_per_step": w.pixels * 3, "d2h_bytes_per_step": w.pixels * 4,
+               "api": "rapid_segment_host (pinned host buffers)"}
+        r.set_profiling(1)
+
+    if rank == 0:
+        peak, peak_src = peaks()
+        pb = phase_bytes(info, w, window)
+        # dominant kernel: the propose sweep (K4); algorithmic bytes per launch / average launch time
+        kbytes = sum(v[0] for v in pb.values())
+        kms = float(prof_ms[rb.K_PROPOSE].sum())
+        klaunch = int(prof_launch[rb.K_PROPOSE].sum())
+        share = kms / max(1e-9, float(prof_ms[[rb.K_PYRAMID, rb.K_SNAPSHOT, rb.K_PROPOSE, rb.K_COMMIT, rb.K_MERGE,
+                                                 rb.K_PREDICT, rb.K_TRANSITION, rb.K_FINAL]].sum()))
+        achieved = kbytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+        px_stage = len(p.block_sizes) - 1
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "kernel": "k_propose (K4 parity-phase sweep), all stages",
+                "bytes_per_launch": round(kbytes / max(1, klaunch)),
+                "avg_launch_ms": round(kms / max(1, klaunch), 4), "launches": klaunch,
+                "share_of_step": round(share, 4), "peak_source": peak_src,
+                "pixel_stage": {"achieved": round(pb[px_stage][0] / (prof_ms[rb.K_PROPOSE][px_stage] / 1e3) / 1e9, 1)
+                                if prof_ms[rb.K_PROPOSE][px_stage] > 0 else None,
+                                "avg_launch_ms": round(float(prof_ms[rb.K_PROPOSE][px_stage]) / max(1, prof_launch[rb.K_PROPOSE][px_stage]), 4)},
+                "phase_set_GBps": round(kbytes / (float(prof_ms[rb.K_PHASESET].sum()) / 1e3) / 1e9, 1)
+                if prof_ms[rb.K_PHASESET].sum() > 0 else None}
+        line = {"metric": METRIC, "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+                "data": "synthetic", "config": config_dict(w, {"parallelism": f"replicas{world}",
+                                                                 "gen_s": round(gen_s, 1)}),
+                "roofline": roof, "e2e": e2e, "gpu_launches": total_launches * args.steps,
+                "clocks": ck,
+                "per_kernel_ms_per_step": {nm: round(float(prof_ms[k].sum()), 3) for k, nm in enumerate(
+                    ["pyramid", "snapshot", "propose", "commit", "merge", "predict", "transition", "final",
+                     "phase_set"])},
+                "stage_propose_ms": [round(float(x), 3) for x in prof_ms[rb.K_PROPOSE][:len(p.block_sizes)]],
+                "stage_sweeps_run": [int(x) for x in info.stage_sweeps_run[:len(p.block_sizes)]],
+                "alive": int(info.alive), "active": int(info.active)}
+        if not args.no_cpu:
+            line["cpu_baseline"] = cpu_baseline(args.config, args.sample)
+        print(json.dumps(line), flush=True)
+    r.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

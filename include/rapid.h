@@ -119,6 +119,8 @@ typedef struct {
   uint64_t stage_victims[RAPID_MAX_STAGES];      /* victims at the stage's merge round */
   uint64_t stage_merges[RAPID_MAX_STAGES];
   uint64_t stage_sweeps_run[RAPID_MAX_STAGES];   /* sweeps actually executed (exact early exit) */
+  uint64_t stage_window_blocks[RAPID_MAX_STAGES];/* blocks within distance 1 of a block whose label
+                                                    can pass the gate (profiling level 2; else 0) */
   uint64_t alive, active;                        /* after the run */
   uint64_t phase[RAPID_MAX_STAGES][RAPID_MAX_SWEEPS][4][RAPID_NCNT]; /* RAPID_C_* */
 } rapid_run_info;
@@ -162,7 +164,8 @@ int rapid_segment_host(rapid_ctx *ctx, const uint8_t *image_host, int32_t H, int
 int rapid_stats(rapid_ctx *ctx, rapid_sp_stat *out_host, uint64_t capacity,
                 rapid_run_info *info_host);
 
-/* Profiling: when enabled, CUDA events bracket every kernel class per stage. */
+/* Profiling: level 1 = CUDA events bracket every kernel class per stage; level 2 also
+ * counts each stage's window blocks (rapid_run_info.stage_window_blocks; extra kernels). */
 int rapid_set_profiling(rapid_ctx *ctx, int enable);
 int rapid_get_profile(rapid_ctx *ctx, rapid_profile *out_host); /* synchronises */
 

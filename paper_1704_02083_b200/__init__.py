@@ -83,6 +83,7 @@ class rapid_run_info(ctypes.Structure):
         ("stage_victims", ctypes.c_uint64 * MAX_STAGES),
         ("stage_merges", ctypes.c_uint64 * MAX_STAGES),
         ("stage_sweeps_run", ctypes.c_uint64 * MAX_STAGES),
+        ("stage_window_blocks", ctypes.c_uint64 * MAX_STAGES),
         ("alive", ctypes.c_uint64), ("active", ctypes.c_uint64),
         ("phase", ctypes.c_uint64 * (MAX_STAGES * MAX_SWEEPS * 4 * NCNT)),
     ]
@@ -262,8 +263,8 @@ class Rapid:
         rapid_stats(self.ctx, out.ctypes.data if K else None, K, info)
         return out, info
 
-    def set_profiling(self, on=True):
-        lib.rapid_set_profiling(self.ctx, 1 if on else 0)
+    def set_profiling(self, level=1):
+        lib.rapid_set_profiling(self.ctx, int(level))
 
     def profile(self):
         pr = rapid_profile()

@@ -86,7 +86,8 @@ struct rapid_ctx {
   size_t hcap = 0;
   unsigned long long *hkeys = nullptr, *candE = nullptr;
   unsigned int *hvals = nullptr;
-  int32_t *hnext = nullptr, *candT = nullptr;
+  int32_t *hnext = nullptr, *candT = nullptr, *candV = nullptr;
+  uint32_t *mlock = nullptr, *res = nullptr;
   Ctl *ctl = nullptr;
   // plan-sized buffers
   DevBuf tab, bsum, maps[2], props, work;
@@ -95,7 +96,8 @@ struct rapid_ctx {
   // occupancy
   int prop_grid[2][2] = {{0, 0}, {0, 0}};
   // profiling
-  bool prof = false;
+  int prof = 0;  // 0 off, 1 events, 2 events + window counting
+  int last_prof = 0;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<ProfEv> evs;
@@ -496,6 +498,10 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
         launch_recount(ra, pixel, grid_k, s, &c->launches);
       }
     }
+    if (c->prof >= 2 && use_work) {  // profiling only: algorithmic window of the gated stage
+      launch_count_window(sd[st], sp, B, M, &ctl->stage_info[st][2], s);
+      c->launches++;
+    }
     if (stop_at(RAPID_STOP_STAGE_START, st, 0, 0)) return RAPID_OK;
     {
       Timer tm(c, s, RAPID_K_PHASESET, st);
@@ -560,7 +566,6 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     }
     if (p->size_mode == RAPID_SIZE_MERGE) {
       Timer tm(c, s, RAPID_K_MERGE, st);
-      cudaMemsetAsync(c->out, 0, sizeof(int32_t) * K, s);
       MergeArgs ma;
       ma.st = sd[st];
       ma.sp = sp;
@@ -581,6 +586,9 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       ma.deg = c->deg;
       ma.deg_total = &ctl->deg_total;
       ma.candT = c->candT;
+      ma.candV = c->candV;
+      ma.mlock = c->mlock;
+      ma.res = c->res;
       ma.candE = c->candE;
       ma.pairs = c->pairs;
       ma.npairs = &ctl->npairs;
@@ -662,6 +670,7 @@ void rapid_free(rapid_ctx *c) {
   void *ptrs[] = {c->sums, c->rc, c->rec, c->init, c->out, c->remap, c->dl[0], c->dl[1], c->head,
                   c->vlist, c->alist, c->pairs, c->alive, c->active, c->victim, c->y, c->dirty,
                   c->deg, c->chunk, c->hkeys, c->candE, c->hvals, c->hnext, c->candT, c->ctl,
+                  c->candV, c->mlock, c->res,
                   c->tab.p, c->bsum.p, c->maps[0].p, c->maps[1].p, c->props.p, c->work.p,
                   c->himg.p, c->hlab.p};
   for (void *q : ptrs)
@@ -700,6 +709,7 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
       (rc = dalloc(c, &c->chunk, K / 1024 + 2)) || (rc = dalloc(c, &c->hkeys, hc)) ||
       (rc = dalloc(c, &c->hvals, hc)) || (rc = dalloc(c, &c->hnext, hc)) ||
       (rc = dalloc(c, &c->candT, hc)) || (rc = dalloc(c, &c->candE, 2 * hc)) ||
+      (rc = dalloc(c, &c->candV, hc)) || (rc = dalloc(c, &c->mlock, K)) || (rc = dalloc(c, &c->res, K)) ||
       (rc = dalloc(c, &c->ctl, 1))) {
     rapid_free(c);
     return rc;
@@ -707,6 +717,8 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   cudaMemset(c->hkeys, 0xff, hc * 8);
   cudaMemset(c->hvals, 0, hc * 4);
   cudaMemset(c->dirty, 0, K * 4);
+  cudaMemset(c->mlock, 0, K * 4);
+  cudaMemset(c->res, 0xff, K * 4);
   cudaMemset(c->rc, 0, K * SUMW * 8);
   for (int px = 0; px < 2; px++)
     for (int gs = 0; gs < 2; gs++) c->prop_grid[px][gs] = propose_occupancy(px, gs);
@@ -734,6 +746,7 @@ int rapid_segment(rapid_ctx *c, const uint8_t *image, int32_t H, int32_t W, cons
   rc = enqueue(c, image, H, W, p, labels_out, s);
   c->stamp_base += (uint32_t)(p->n_stages * p->sweeps * 4 + 8);
   c->last = *p;
+  c->last_prof = c->prof;
   c->have_run = true;
   c->last_stream = s;
   if (rc) return rc;
@@ -821,6 +834,9 @@ int rapid_stats(rapid_ctx *c, rapid_sp_stat *out, uint64_t capacity, rapid_run_i
         if (com == 0) break;
       }
       info->stage_sweeps_run[s] = run;
+      if (c->last_prof >= 2)
+        info->stage_window_blocks[s] =
+            work ? h->stage_info[s][2] : (uint64_t)P.st[s].nbx * P.st[s].nby * P.B;
     }
     memcpy(info->phase, h->cnt, sizeof(info->phase));
     std::vector<uint8_t> alive(K), active(K);
@@ -840,7 +856,7 @@ int rapid_stats(rapid_ctx *c, rapid_sp_stat *out, uint64_t capacity, rapid_run_i
 
 int rapid_set_profiling(rapid_ctx *c, int enable) {
   if (!c) return RAPID_E_ARG;
-  c->prof = enable != 0;
+  c->prof = enable < 0 ? 0 : (enable > 2 ? 2 : enable);
   return RAPID_OK;
 }
 

@@ -658,48 +658,72 @@ __global__ void k_merge_fill(const MergeArgs a) {
       a.candE[2 * (off + k) + 1] = (unsigned long long)E;
       c++;
     }
+    for (unsigned k = 0; k < c; k++) a.candV[off + k] = A;
   }
 }
 
-// O7 steps 3-4: victims in ascending id, first unlocked candidate wins; locks in smem bits
-__global__ void k_merge_sequential(const MergeArgs a, int use_smem) {
+// O7 steps 3-4.  The sequential rule — victims in ascending id; an unlocked victim takes its
+// first unlocked candidate (sorted by (dE_m, T)); both get locked — is exactly the greedy
+// maximal matching over the edges (A, T) taken in CSR order (victims ascending, candidates
+// sorted).  It is computed with deterministic reservations: every pending edge whose ends
+// are both free reserves both ends with atomicMin(edge id); an edge holding both of its
+// reservations is the earliest pending edge at both ends, so the sequential order would
+// take it too.  Rounds repeat until no edge is pending; the result is order-independent.
+// mlock[] (per superpixel) and res[] (reservations) are zero / ~0 outside this kernel.
+__global__ void __launch_bounds__(1024) k_merge_match(const MergeArgs a) {
   if (*a.victim_any == 0u) return;
-  extern __shared__ unsigned lockbits[];
-  const int nwords = (a.K + 31) / 32;
-  if (use_smem)
-    for (int w = threadIdx.x; w < nwords; w += blockDim.x) lockbits[w] = 0u;
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  uint32_t *glock = reinterpret_cast<uint32_t *>(a.sp.out);  // reuse: out[] is free here
-  auto locked = [&](int k) -> bool {
-    return use_smem ? ((lockbits[k >> 5] >> (k & 31)) & 1u) : (glock[k] != 0u);
-  };
-  auto lock = [&](int k) {
-    if (use_smem) lockbits[k >> 5] |= 1u << (k & 31);
-    else glock[k] = 1u;
-  };
-  const unsigned nv = *a.total;
-  unsigned np = 0;
-  for (unsigned i = 0; i < nv; i++) {
-    const int A = a.vlist[i];
-    if (locked(A)) continue;
-    const unsigned e = a.deg[i + 1];
-    for (unsigned p = a.deg[i]; p < e; p++) {
+  __shared__ int s_any;
+  __shared__ unsigned s_np;
+  const unsigned ne = a.deg[*a.total];
+  if (threadIdx.x == 0) s_np = 0;
+  while (true) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_any = 0;
+    __syncthreads();
+    int any = 0;
+    for (unsigned p = threadIdx.x; p < ne; p += blockDim.x) {
       const int T = a.candT[p];
-      if (T < 0) break;  // infeasible entries sort last
-      if (locked(T)) continue;
-      a.pairs[2 * np] = A;
-      a.pairs[2 * np + 1] = T;
-      np++;
-      lock(A);
-      lock(T);
-      break;
+      if (T < 0) continue;
+      const int V = a.candV[p];
+      if (a.mlock[V] || a.mlock[T]) {
+        a.candT[p] = -1;  // an end is taken: dropped for good
+        continue;
+      }
+      atomicMin(&a.res[V], p);
+      atomicMin(&a.res[T], p);
+      any = 1;
+    }
+    if (any) s_any = 1;
+    __syncthreads();
+    if (!s_any) break;
+    for (unsigned p = threadIdx.x; p < ne; p += blockDim.x) {
+      const int T = a.candT[p];
+      if (T < 0) continue;
+      const int V = a.candV[p];
+      if (a.res[V] == p && a.res[T] == p) {
+        a.mlock[V] = 1u;
+        a.mlock[T] = 1u;
+        a.res[T] = 0xffffffffu;  // V's reservation is released below
+        const unsigned q = atomicAdd(&s_np, 1u);
+        a.pairs[2 * q] = V;
+        a.pairs[2 * q + 1] = T;
+        a.candT[p] = -1;
+      }
+    }
+    __syncthreads();
+    for (unsigned p = threadIdx.x; p < ne; p += blockDim.x) {  // release reservations
+      const int T = a.candT[p];
+      const int V = a.candV[p];
+      a.res[V] = 0xffffffffu;
+      if (T >= 0) a.res[T] = 0xffffffffu;
     }
   }
-  *a.npairs = np;
-  a.stage_info[0] += nv;
-  a.stage_info[1] += np;
-  if (np) *a.remap_pending = 1u;
+  if (threadIdx.x == 0) {
+    *a.npairs = s_np;
+    a.stage_info[0] += *a.total;
+    a.stage_info[1] += s_np;
+    if (s_np) *a.remap_pending = 1u;
+  }
 }
 
 __global__ void k_merge_apply(const MergeArgs a) {
@@ -716,24 +740,21 @@ __global__ void k_merge_apply(const MergeArgs a) {
     a.sp.active[A] = 0;
     a.sp.y[A] = 0;
     a.sp.remap[A] = T % a.M;  // local id of the target
+    a.mlock[A] = 0u;
+    a.mlock[T] = 0u;
   }
 }
 
-__global__ void k_merge_cleanup(const MergeArgs a, int glock_clear) {
+__global__ void k_merge_cleanup(const MergeArgs a) {
   if (*a.victim_any == 0u) return;
   const unsigned nv = *a.total;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x) {
     const int A = a.vlist[i];
     a.sp.victim[A] = 0;
     for (int h = a.head[A]; h >= 0; h = a.hnext[h]) {
-      if (glock_clear) {
-        const int T = (int)(a.hkeys[h] & 0xffffffffull);
-        reinterpret_cast<uint32_t *>(a.sp.out)[T] = 0u;
-      }
       a.hkeys[h] = HEMPTY;
       a.hvals[h] = 0u;
     }
-    if (glock_clear) reinterpret_cast<uint32_t *>(a.sp.out)[A] = 0u;
   }
 }
 
@@ -899,6 +920,37 @@ __global__ void k_final_remap(const FinalArgs a) {
   }
 }
 
+// ------------------------------------------------- profiling: algorithmic window blocks
+// blocks within Chebyshev distance 1 of a block whose label can pass the active gate
+__global__ void k_count_window(const StageDev st, const SpDev sp, int B, int M,
+                               unsigned long long *out) {
+  const size_t nper = (size_t)st.nbx * st.nby;
+  const size_t n = nper * B;
+  unsigned c = 0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t base = blockIdx.x * (size_t)blockDim.x; base < n; base += stride) {
+    const size_t t = base + threadIdx.x;
+    bool hit = false;
+    if (t < n) {
+      const int img = (int)(t / nper);
+      const size_t r = t - (size_t)img * nper;
+      const int gy = (int)(r / st.nbx), gx = (int)(r - (size_t)gy * st.nbx);
+      const int32_t *map = st.map + (size_t)img * nper;
+      for (int dy = -1; dy <= 1 && !hit; dy++)
+        for (int dx = -1; dx <= 1 && !hit; dx++) {
+          const int x = gx + dx, y = gy + dy;
+          if (x < 0 || y < 0 || x >= st.nbx || y >= st.nby) continue;
+          hit = sp.active[img * M + map[(size_t)y * st.nbx + x]] != 0;
+        }
+    }
+    c += __popc(__ballot_sync(FULL, hit));
+  }
+  if (lane_id() == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+void launch_count_window(const StageDev &st, const SpDev &sp, int B, int M, unsigned long long *out,
+                         cudaStream_t s);
+
 // =================================================================== launch wrappers
 static int grid_for(size_t n, int threads, int cap = 148 * 16) {
   size_t g = (n + threads - 1) / threads;
@@ -971,13 +1023,9 @@ void launch_merge_round(const MergeArgs &a, int grid, cudaStream_t s, int *nlaun
   k_merge_degree<<<grid, 256, 0, s>>>(a);
   k_merge_scan_deg<<<1, 1024, 0, s>>>(a);
   k_merge_fill<<<grid, 256, 0, s>>>(a);
-  const size_t lock_bytes = (size_t)((a.K + 31) / 32) * 4;
-  const int use_smem = lock_bytes <= 200 * 1024;
-  if (use_smem && lock_bytes > 48 * 1024)
-    cudaFuncSetAttribute(k_merge_sequential, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lock_bytes);
-  k_merge_sequential<<<1, 256, use_smem ? lock_bytes : 0, s>>>(a, use_smem);
+  k_merge_match<<<1, 1024, 0, s>>>(a);
   k_merge_apply<<<grid, 256, 0, s>>>(a);
-  k_merge_cleanup<<<grid, 256, 0, s>>>(a, use_smem ? 0 : 1);
+  k_merge_cleanup<<<grid, 256, 0, s>>>(a);
   k_merge_done<<<1, 1, 0, s>>>(a);
   *nlaunch += 12;
 }
@@ -1009,6 +1057,12 @@ void launch_recount(const RecountArgs &a, bool pixel, int grid, cudaStream_t s, 
   k_recount_check<<<grid_for(a.K, 256), 256, 0, s>>>(a);
   *nlaunch += 2;
   (void)grid;
+}
+
+void launch_count_window(const StageDev &st, const SpDev &sp, int B, int M, unsigned long long *out,
+                         cudaStream_t s) {
+  const size_t n = (size_t)st.nbx * st.nby * B;
+  k_count_window<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(st, sp, B, M, out);
 }
 
 void launch_final(const FinalArgs &a, bool upsample, cudaStream_t s) {

@@ -55,8 +55,11 @@ struct MergeArgs {
   // candidates
   unsigned int *deg;         // [victims] -> offsets (in place scan)
   unsigned int *deg_total;
-  int32_t *candT;
-  unsigned long long *candE; // int128 as (hi, lo) pairs, bias-encoded for unsigned compare
+  int32_t *candT;            // candidate target (global id), -1 = infeasible / resolved
+  int32_t *candV;            // candidate's victim
+  unsigned long long *candE; // dE_m as int128 (hi, lo)
+  uint32_t *mlock;           // [K] matched flags (zero outside the round)
+  uint32_t *res;             // [K] reservations (~0 outside the round)
   int32_t *pairs;            // merges (A, T)
   unsigned int *npairs;
   unsigned long long *stage_info; // [4]: victims, merges, active tiles, -
@@ -130,5 +133,7 @@ void launch_transition(const TransArgs &a, cudaStream_t s);
 void launch_recount(const RecountArgs &a, bool pixel, int grid, cudaStream_t s, int *nlaunch);
 void launch_final(const FinalArgs &a, bool upsample, cudaStream_t s);
 int propose_occupancy(bool pixel, bool gated);
+void launch_count_window(const StageDev &st, const SpDev &sp, int B, int M, unsigned long long *out,
+                         cudaStream_t s);
 
 }  // namespace rapid

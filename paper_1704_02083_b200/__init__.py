@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librapid.so")
+LIB_PATH = os.environ.get("RAPID_LIB", os.path.join(_HERE, "librapid.so"))  # override: A/B builds
 
 MAX_STAGES = 12
 MAX_SWEEPS = 64

@@ -4,6 +4,7 @@
 // rapid_init fails.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -95,6 +96,7 @@ struct rapid_ctx {
   DevBuf himg, hlab;
   // occupancy
   int prop_grid[2][2] = {{0, 0}, {0, 0}};
+  bool use_tma = true;  // RAPID_NO_TMA=1 forces the LDG tile loader (A/B testing)
   // profiling
   int prof = 0;  // 0 off, 1 events, 2 events + window counting
   int last_prof = 0;
@@ -330,7 +332,7 @@ int build_plan(rapid_ctx *c, int H, int W, const rapid_params *p) {
   if ((rc = ensure(c, c->bsum, N.bsum_total * 8))) return rc;
   if ((rc = ensure(c, c->maps[0], N.map_max * 4))) return rc;
   if ((rc = ensure(c, c->maps[1], N.map_max * 4))) return rc;
-  if ((rc = ensure(c, c->props, N.props_max * 8))) return rc;
+  if ((rc = ensure(c, c->props, N.props_max * 16))) return rc;
   if ((rc = ensure(c, c->work, N.tiles_max * 4))) return rc;
   cudaError_t e = cudaMemcpy(c->tab.p, N.tab.data(), N.tab.size() * 4, cudaMemcpyHostToDevice);
   if ((rc = cuda_check(c, e, "upload tables"))) return rc;
@@ -417,7 +419,15 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
   cudaMemsetAsync(ctl, 0, sizeof(Ctl), s);
 
   StageDev sd[MAXS];
-  for (int st = 0; st < nst; st++) sd[st] = stage_dev(c, st, labels);
+  struct alignas(64) TMap {
+    unsigned char b[128];  // CUtensorMap
+  };
+  TMap tmaps[MAXS];
+  bool has_tmap[MAXS];
+  for (int st = 0; st < nst; st++) {
+    sd[st] = stage_dev(c, st, labels);
+    has_tmap[st] = c->use_tma && make_label_tmap(tmaps[st].b, sd[st].map, sd[st].nbx, sd[st].nby, B);
+  }
   const SpDev sp = sp_dev(c);
   const int32_t *T = (const int32_t *)c->tab.p;
 
@@ -533,7 +543,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           pa.lam_b = p->lambda_b_q16;
           pa.worklist = use_work ? (const int32_t *)c->work.p : nullptr;
           pa.nwork = &ctl->nwork[st];
-          pa.props = (unsigned long long *)c->props.p;
+          pa.props = (uint4 *)c->props.p;
           pa.prop_count = &ctl->prop_count[g];
           pa.dlist = c->dl[g & 1];
           pa.dcount = &ctl->dcount[g];
@@ -544,7 +554,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           if (gated_sz) cudaMemsetAsync(c->out, 0, sizeof(int32_t) * K, s);
           {
             Timer t2(c, s, RAPID_K_PROPOSE, st);
-            launch_propose(pa, pixel, c->sm_count * c->prop_grid[pixel][gated_sz], s);
+            launch_propose(pa, has_tmap[st] ? tmaps[st].b : nullptr, pixel,
+                           c->sm_count * c->prop_grid[pixel][gated_sz], s);
             c->launches++;
           }
           if (gated_sz) {
@@ -722,6 +733,10 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   cudaMemset(c->rc, 0, K * SUMW * 8);
   for (int px = 0; px < 2; px++)
     for (int gs = 0; gs < 2; gs++) c->prop_grid[px][gs] = propose_occupancy(px, gs);
+  {
+    const char *e = getenv("RAPID_NO_TMA");
+    c->use_tma = !(e && e[0] == '1');
+  }
   rc = cuda_check(c, cudaDeviceSynchronize(), "rapid_init");
   if (rc) {
     rapid_free(c);

@@ -54,6 +54,45 @@ struct SpDev {
   int32_t *remap;            // [K]
 };
 
+struct RecV {
+  long long c0, c1, c2, mx, my;
+};
+__device__ __forceinline__ RecV rec_vals(const Rec &r) {
+  RecV v;
+  v.c0 = r.cq01 & 0xffffu;
+  v.c1 = r.cq01 >> 16;
+  v.c2 = r.cq2f & 0xffffu;
+  v.mx = r.mux;
+  v.my = r.muy;
+  return v;
+}
+
+// Exact early exit (DESIGN §2 A25): a sweep with zero commits leaves labels and sums
+// unchanged, so every later sweep of the stage would repeat it identically.
+__device__ __forceinline__ bool sweep_skipped(const unsigned long long *prev) {
+  if (prev == nullptr) return false;
+  return (prev[0 * NCNT + 4] + prev[1 * NCNT + 4] + prev[2 * NCNT + 4] + prev[3 * NCNT + 4]) == 0ull;
+}
+
+// Yokoi 4-connectivity number == 1 on the 8-ring (N,NE,E,SE,S,SW,W,NW = bits 0..7):
+// C4 = sum_{k in N,E,S,W} x_k (1 - x_{k+1} x_{k+2})   (E_topo; DESIGN A9)
+__device__ __forceinline__ bool simple_point(unsigned m) {
+  const unsigned r = m | (m << 8);  // ring wrap
+  unsigned c = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    const unsigned xk = (r >> k) & 1u, x1 = (r >> (k + 1)) & 1u, x2 = (r >> (k + 2)) & 1u;
+    c += xk & ~(x1 & x2) & 1u;
+  }
+  return c == 1u;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
 __device__ __forceinline__ long long warp_sum_ll(long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);

@@ -19,32 +19,6 @@ namespace rapid {
 typedef __int128 i128;
 
 // ------------------------------------------------------------------------------- helpers
-__device__ __forceinline__ bool sweep_skipped(const unsigned long long *prev) {
-  // Exact early exit (DESIGN §2 A25): a sweep with zero commits leaves labels and sums
-  // unchanged, so every later sweep of the stage would repeat it identically.
-  if (prev == nullptr) return false;
-  return (prev[0 * NCNT + 4] + prev[1 * NCNT + 4] + prev[2 * NCNT + 4] + prev[3 * NCNT + 4]) == 0ull;
-}
-
-// Yokoi 4-connectivity number == 1 on the 8-ring (N,NE,E,SE,S,SW,W,NW = bits 0..7):
-// C4 = sum_{k in N,E,S,W} x_k (1 - x_{k+1} x_{k+2})   (E_topo; DESIGN A9)
-__device__ __forceinline__ bool simple_point(unsigned m) {
-  const unsigned r = m | (m << 8);  // ring wrap
-  unsigned c = 0;
-#pragma unroll
-  for (int k = 0; k < 8; k += 2) {
-    const unsigned xk = (r >> k) & 1u, x1 = (r >> (k + 1)) & 1u, x2 = (r >> (k + 2)) & 1u;
-    c += xk & ~(x1 & x2) & 1u;
-  }
-  return c == 1u;
-}
-
-__device__ __forceinline__ unsigned lanemask_lt() {
-  unsigned m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
 // ------------------------------------------------------------------ K2: initial state
 __global__ void k_init_sp(const InitArgs a) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.K; k += gridDim.x * blockDim.x) {
@@ -172,233 +146,6 @@ __global__ void k_snapshot(const SnapArgs a) {
     make_rec(a.sp, a.list ? a.list[i] : i);
 }
 
-// ------------------------------------------------------------------ K4: propose
-struct RecV {
-  long long c0, c1, c2, mx, my;
-};
-__device__ __forceinline__ RecV rec_vals(const Rec &r) {
-  RecV v;
-  v.c0 = r.cq01 & 0xffffu;
-  v.c1 = r.cq01 >> 16;
-  v.c2 = r.cq2f & 0xffffu;
-  v.mx = r.mux;
-  v.my = r.muy;
-  return v;
-}
-
-// 2^(-16) x the oracle's weighted dE (same sign, same order): exact integer Eq. 1 difference
-// of relabelling a pixel set with data d from A to B under the frozen means.
-__device__ __forceinline__ i128 delta_e(const RecV &ra, const RecV &rb, const long long d[6],
-                                        long long dB2, long long lam_pos, long long lam_b) {
-  const long long n = d[0];
-  long long dC = (rb.c0 - ra.c0) * (n * (rb.c0 + ra.c0) - (d[1] << (FRAC + 1))) +
-                 (rb.c1 - ra.c1) * (n * (rb.c1 + ra.c1) - (d[2] << (FRAC + 1)));
-  i128 dCw = (i128)dC + (i128)((rb.c2 - ra.c2) * (n * (rb.c2 + ra.c2) - (d[3] << (FRAC + 1))));
-  const long long dP = (rb.mx - ra.mx) * (n * (rb.mx + ra.mx) - (d[4] << (FRAC + 1))) +
-                       (rb.my - ra.my) * (n * (rb.my + ra.my) - (d[5] << (FRAC + 1)));
-  return (dCw << 16) + (i128)lam_pos * (i128)dP + ((i128)(lam_b * dB2) << 16);
-}
-
-template <bool PIXEL, bool GATED>
-__global__ void __launch_bounds__(PROP_THREADS) k_propose(const PhaseArgs a) {
-  if (sweep_skipped(a.prev)) return;
-  __shared__ int32_t tl[TY + 2][TX + 3];
-  const int lane = lane_id();
-  const int li = 2 * (threadIdx.x & 31) + a.cx;  // candidate block within the tile
-  const int lj = 2 * (threadIdx.x >> 5) + a.cy;
-  const int nbx = a.st.nbx, nby = a.st.nby;
-  const unsigned ntiles =
-      a.worklist ? *a.nwork : (unsigned)(a.st.tiles_x * a.st.tiles_y) * (unsigned)a.B;
-  unsigned c_cand = 0, c_topo = 0, c_prop = 0, c_srej = 0, c_commit = 0;
-
-  for (unsigned w = blockIdx.x; w < ntiles; w += gridDim.x) {
-    const unsigned t = a.worklist ? (unsigned)a.worklist[w] : w;
-    const int tx = (int)(t % (unsigned)a.st.tiles_x);
-    const unsigned rr0 = t / (unsigned)a.st.tiles_x;
-    const int ty = (int)(rr0 % (unsigned)a.st.tiles_y);
-    const int img = (int)(rr0 / (unsigned)a.st.tiles_y);
-    const int gx0 = tx * TX, gy0 = ty * TY;
-    int32_t *map = a.st.map + (size_t)img * nby * nbx;
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < (TY + 2) * (TX + 2); idx += PROP_THREADS) {
-      const int r = idx / (TX + 2), c = idx - r * (TX + 2);
-      const int gy = gy0 + r - 1, gx = gx0 + c - 1;
-      tl[r][c] = (gx >= 0 && gx < nbx && gy >= 0 && gy < nby) ? map[(size_t)gy * nbx + gx] : -1;
-    }
-    __syncthreads();
-
-    const int gx = gx0 + li, gy = gy0 + lj;
-    const bool valid = gx < nbx && gy < nby;
-    int A = -1;
-    int nq[4] = {-1, -1, -1, -1};
-    bool bnd = false;
-    if (valid) {
-      A = tl[lj + 1][li + 1];
-      nq[0] = tl[lj][li + 1];      // N
-      nq[1] = tl[lj + 1][li + 2];  // E
-      nq[2] = tl[lj + 2][li + 1];  // S
-      nq[3] = tl[lj + 1][li];      // W
-      bnd = (nq[0] >= 0 && nq[0] != A) | (nq[1] >= 0 && nq[1] != A) |
-            (nq[2] >= 0 && nq[2] != A) | (nq[3] >= 0 && nq[3] != A);
-    }
-    const int kb = img * a.M;
-    bool cand = false, topo = false, prop = false, srej = false;
-    int Bm = -1;
-    long long d[6] = {0, 0, 0, 0, 0, 0};
-    if (bnd) {
-      bool gate = true;
-      if (a.gating == 1) {
-        gate = a.sp.active[kb + A] != 0;
-      } else if (a.gating == 2) {  // Eq. 7 at block level
-        const int8_t yA = a.sp.y[kb + A];
-        gate = false;
-#pragma unroll
-        for (int q = 0; q < 4; q++)
-          if (nq[q] >= 0 && nq[q] != A && a.sp.y[kb + nq[q]] != yA) gate = true;
-      }
-      if (gate) {
-        cand = true;
-        unsigned m = 0;
-        m |= (unsigned)(tl[lj][li + 1] == A) << 0;
-        m |= (unsigned)(tl[lj][li + 2] == A) << 1;
-        m |= (unsigned)(tl[lj + 1][li + 2] == A) << 2;
-        m |= (unsigned)(tl[lj + 2][li + 2] == A) << 3;
-        m |= (unsigned)(tl[lj + 2][li + 1] == A) << 4;
-        m |= (unsigned)(tl[lj + 2][li] == A) << 5;
-        m |= (unsigned)(tl[lj + 1][li] == A) << 6;
-        m |= (unsigned)(tl[lj][li] == A) << 7;
-        if (simple_point(m)) {
-          topo = true;
-          long long e[4];
-          if (PIXEL) {
-            block_data_pix(a.image, a.H, a.W, img, gx, gy, d);
-            e[0] = e[1] = e[2] = e[3] = 1;
-          } else {
-            block_data_blk(a.st, img, gx, gy, d);
-            const long long bw = a.st.xs[gx + 1] - a.st.xs[gx], bh = a.st.ys[gy + 1] - a.st.ys[gy];
-            e[0] = bw; e[1] = bh; e[2] = bw; e[3] = bh;
-          }
-          const Rec recA = a.sp.rec[kb + A];
-          const RecV ra = rec_vals(recA);
-          bool have = false;
-          i128 bestE = 0;
-          int bestB = 0;
-#pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const int B = nq[q];
-            bool skip = (B < 0) || (B == A);
-#pragma unroll
-            for (int r = 0; r < q; r++) skip |= (nq[r] == B);
-            if (skip) continue;
-            long long dB2 = 0;
-#pragma unroll
-            for (int r = 0; r < 4; r++)
-              if (nq[r] >= 0) dB2 += e[r] * ((long long)(nq[r] != B) - (long long)(nq[r] != A));
-            const RecV rb = rec_vals(a.sp.rec[kb + B]);
-            const i128 E = delta_e(ra, rb, d, 2 * dB2, a.lam_pos, a.lam_b);
-            if (!have || E < bestE || (E == bestE && B < bestB)) {
-              have = true;
-              bestE = E;
-              bestB = B;
-            }
-          }
-          if (have && bestE < 0) {
-            if (a.size_mode != 0 &&
-                ((long long)recA.n - d[0]) * a.l_den < a.l_num * (long long)recA.init) {
-              srej = true;  // A12: the desired move would leave A below l * InitSize
-              if (a.size_mode == 2) {
-                a.sp.victim[kb + A] = 1;
-                *a.victim_any = 1u;
-              }
-            } else {
-              prop = true;
-              Bm = bestB;
-            }
-          }
-        }
-      }
-    }
-    c_cand += __popc(__ballot_sync(FULL, cand));
-    c_topo += __popc(__ballot_sync(FULL, topo));
-    c_srej += __popc(__ballot_sync(FULL, srej));
-    const unsigned pm = __ballot_sync(FULL, prop);
-    c_prop += __popc(pm);
-    if (pm) {
-      if (!GATED) {  // size_mode NONE: commit in place (no budget to check)
-        if (prop) map[(size_t)gy * nbx + gx] = Bm;
-        agg_sums(prop, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp, a.dlist, a.dcount);
-        agg_sums(prop, kb + Bm, d, false, a.sp.sums, a.sp.dirty, a.stamp, a.dlist, a.dcount);
-        c_commit += __popc(pm);
-      } else {
-        agg_add_i32(prop, kb + A, (int)d[0], a.sp.out);
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(a.prop_count, (unsigned long long)__popc(pm));
-        base = __shfl_sync(FULL, base, 0);
-        if (prop) {
-          const size_t idx = ((size_t)img * nby + gy) * nbx + gx;
-          a.props[base + __popc(pm & lanemask_lt())] =
-              (unsigned long long)idx | ((unsigned long long)(unsigned)Bm << 32);
-        }
-      }
-    }
-  }
-  if (lane == 0) {
-    if (c_cand) atomicAdd(&a.cnt[0], (unsigned long long)c_cand);
-    if (c_topo) atomicAdd(&a.cnt[1], (unsigned long long)c_topo);
-    if (c_prop) atomicAdd(&a.cnt[2], (unsigned long long)c_prop);
-    if (c_srej) atomicAdd(&a.cnt[3], (unsigned long long)c_srej);
-    if (c_commit) atomicAdd(&a.cnt[4], (unsigned long long)c_commit);
-  }
-}
-
-// ------------------------------------------------------------------ K5: commit
-template <bool PIXEL>
-__global__ void __launch_bounds__(256) k_commit(const PhaseArgs a) {
-  if (sweep_skipped(a.prev)) return;
-  const unsigned long long n = *a.prop_count;
-  const size_t nper = (size_t)a.st.nbx * a.st.nby;
-  unsigned c_commit = 0, c_rej = 0;
-  for (unsigned long long base = blockIdx.x * 256ull; base < n; base += gridDim.x * 256ull) {
-    const unsigned long long i = base + threadIdx.x;
-    const bool valid = i < n;
-    bool ok = false, rej = false;
-    int A = 0, B = 0, kb = 0;
-    long long d[6] = {0, 0, 0, 0, 0, 0};
-    size_t idx = 0;
-    if (valid) {
-      const unsigned long long pr = a.props[i];
-      idx = (size_t)(pr & 0xffffffffull);
-      B = (int)(pr >> 32);
-      const int img = (int)(idx / nper);
-      const size_t r = idx - (size_t)img * nper;
-      const int gy = (int)(r / a.st.nbx), gx = (int)(r - (size_t)gy * a.st.nbx);
-      kb = img * a.M;
-      A = a.st.map[idx];
-      const Rec ra = a.sp.rec[kb + A];
-      // O6' all-or-nothing budget: total proposed outflow must keep A >= l * InitSize (A19)
-      ok = !(((long long)ra.n - (long long)a.sp.out[kb + A]) * a.l_den < a.l_num * (long long)ra.init);
-      if (ok) {
-        if (PIXEL) block_data_pix(a.image, a.H, a.W, img, gx, gy, d);
-        else block_data_blk(a.st, img, gx, gy, d);
-        a.st.map[idx] = B;
-      } else {
-        rej = true;
-        if (a.size_mode == 2) {
-          a.sp.victim[kb + A] = 1;
-          *a.victim_any = 1u;
-        }
-      }
-    }
-    agg_sums(ok, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp, a.dlist, a.dcount);
-    agg_sums(ok, kb + B, d, false, a.sp.sums, a.sp.dirty, a.stamp, a.dlist, a.dcount);
-    c_commit += __popc(__ballot_sync(FULL, ok));
-    c_rej += __popc(__ballot_sync(FULL, rej));
-  }
-  if (lane_id() == 0) {
-    if (c_commit) atomicAdd(&a.cnt[4], (unsigned long long)c_commit);
-    if (c_rej) atomicAdd(&a.cnt[5], (unsigned long long)c_rej);
-  }
-}
 
 // ------------------------------------------------------- ordered compaction of u8 flags
 // chunk = 1024 flags per CTA of 256 threads (4 consecutive flags per thread)
@@ -988,28 +735,6 @@ void launch_stats0(const InitArgs &a, cudaStream_t s) {
 
 void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s) {
   k_snapshot<<<grid, 256, 0, s>>>(a);
-}
-
-int propose_occupancy(bool pixel, bool gated) {
-  int nb = 0;
-  if (pixel && gated) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propose<true, true>, PROP_THREADS, 0);
-  if (pixel && !gated) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propose<true, false>, PROP_THREADS, 0);
-  if (!pixel && gated) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propose<false, true>, PROP_THREADS, 0);
-  if (!pixel && !gated) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_propose<false, false>, PROP_THREADS, 0);
-  return nb < 1 ? 1 : nb;
-}
-
-void launch_propose(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
-  const bool gated = a.size_mode != 0;
-  if (pixel && gated) k_propose<true, true><<<grid, PROP_THREADS, 0, s>>>(a);
-  else if (pixel) k_propose<true, false><<<grid, PROP_THREADS, 0, s>>>(a);
-  else if (gated) k_propose<false, true><<<grid, PROP_THREADS, 0, s>>>(a);
-  else k_propose<false, false><<<grid, PROP_THREADS, 0, s>>>(a);
-}
-
-void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
-  if (pixel) k_commit<true><<<grid, 256, 0, s>>>(a);
-  else k_commit<false><<<grid, 256, 0, s>>>(a);
 }
 
 void launch_merge_round(const MergeArgs &a, int grid, cudaStream_t s, int *nlaunch) {

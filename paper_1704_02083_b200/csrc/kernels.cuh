@@ -17,7 +17,7 @@ struct PhaseArgs {
   long long lam_pos, lam_b;  // Q16
   const int32_t *worklist;   // null: every tile of the stage
   const unsigned int *nwork; // device count of the worklist
-  unsigned long long *props; // proposals: stage-map index | B << 32
+  uint4 *props;              // proposals {stage-map index, A, B, packed RGB (pixel stage)}
   unsigned long long *prop_count;
   int32_t *dlist;            // dirty list of this phase
   unsigned int *dcount;
@@ -125,8 +125,12 @@ void launch_pyramid_up(const StageDev &parent, const StageDev &child, int B, uin
 void launch_init_map0(const InitArgs &a, cudaStream_t s);
 void launch_stats0(const InitArgs &a, cudaStream_t s);
 void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s);
-void launch_propose(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
+// K4: tmap = TMA descriptor of the stage map (CUtensorMap*), or null for the LDG loader
+void launch_propose(const PhaseArgs &a, const void *tmap, bool pixel, int grid, cudaStream_t s);
 void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
+// encode a 3-D TMA descriptor {nbx, nby, B} of int32 with box {TX+4, TY+2, 1};
+// false when nbx*4 is not a multiple of 16 B (the LDG loader is used then)
+bool make_label_tmap(void *tmap64B, int32_t *base, int nbx, int nby, int B);
 void launch_merge_round(const MergeArgs &a, int grid, cudaStream_t s, int *nlaunch);
 void launch_predict(const PredictArgs &a, int grid, cudaStream_t s, int *nlaunch);
 void launch_transition(const TransArgs &a, cudaStream_t s);

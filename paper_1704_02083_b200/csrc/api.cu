@@ -20,7 +20,6 @@ struct Ctl {  // per-segmentation device control block (zeroed at the start of e
   unsigned long long cnt[MAXS][MAXSW][4][NCNT];
   unsigned long long prop_count[MAXS * MAXSW * 4];
   unsigned long long stage_info[MAXS][4];
-  unsigned int dcount[MAXS * MAXSW * 4 + 4];
   unsigned int victim_any[MAXS];
   unsigned int remap_pending[MAXS];
   unsigned int nwork[MAXS];
@@ -77,7 +76,7 @@ struct rapid_ctx {
   // per-superpixel arrays (cap_sp)
   unsigned long long *sums = nullptr, *rc = nullptr;
   Rec *rec = nullptr;
-  int32_t *init = nullptr, *out = nullptr, *remap = nullptr, *dl[2] = {nullptr, nullptr};
+  int32_t *init = nullptr, *out = nullptr, *remap = nullptr;
   int32_t *head = nullptr, *vlist = nullptr, *alist = nullptr, *pairs = nullptr;
   uint8_t *alive = nullptr, *active = nullptr, *victim = nullptr;
   int8_t *y = nullptr;
@@ -351,6 +350,8 @@ StageDev stage_dev(rapid_ctx *c, int s, int32_t *labels_out) {
   d.b = S.b;
   d.tiles_x = S.tiles_x;
   d.tiles_y = S.tiles_y;
+  d.fd_tx = make_fastdiv((uint32_t)S.tiles_x);
+  d.fd_ty = make_fastdiv((uint32_t)S.tiles_y);
   d.xs = T + S.o_xs;
   d.ys = T + S.o_ys;
   d.px = T + S.o_px;
@@ -478,6 +479,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     fa.bxp = nullptr; fa.byp = nullptr;
     fa.remap_pending = &ctl->remap_pending[st];
     fa.labels = sd[st].map;
+    fa.worklist = nullptr;
+    fa.nwork = nullptr;
     launch_final(fa, false, s);
   };
 
@@ -517,7 +520,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       Timer tm(c, s, RAPID_K_PHASESET, st);
       {
         Timer t2(c, s, RAPID_K_SNAPSHOT, st);
-        SnapArgs sa{sp, K, nullptr, nullptr};
+        SnapArgs sa{sp, K, 0u};
         launch_snapshot(sa, grid_k, s);
         c->launches++;
       }
@@ -525,7 +528,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
         for (int ph = 0; ph < 4; ph++, g++) {
           if (!(t == 0 && ph == 0)) {
             Timer t2(c, s, RAPID_K_SNAPSHOT, st);
-            SnapArgs sa{sp, K, c->dl[(g - 1) & 1], &ctl->dcount[g - 1]};
+            SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1)};
             launch_snapshot(sa, grid_k, s);
             c->launches++;
           }
@@ -545,8 +548,6 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           pa.nwork = &ctl->nwork[st];
           pa.props = (uint4 *)c->props.p;
           pa.prop_count = &ctl->prop_count[g];
-          pa.dlist = c->dl[g & 1];
-          pa.dcount = &ctl->dcount[g];
           pa.stamp = c->stamp_base + (uint32_t)g;
           pa.cnt = &ctl->cnt[st][t][ph][0];
           pa.prev = t > 0 ? &ctl->cnt[st][t - 1][0][0] : nullptr;
@@ -560,7 +561,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           }
           if (gated_sz) {
             Timer t2(c, s, RAPID_K_COMMIT, st);
-            launch_commit(pa, pixel, grid_k, s);
+            launch_commit(pa, pixel, c->sm_count * 8, s);  // latency-bound gathers: full occupancy
             c->launches++;
           }
           if (stop_at(RAPID_STOP_PHASE, st, t, ph)) return RAPID_OK;
@@ -570,7 +571,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     {  // snapshot of the last phase's changes (merge round / prediction read it)
       Timer t2(c, s, RAPID_K_SNAPSHOT, st);
       if (g > 0) {
-        SnapArgs sa{sp, K, c->dl[(g - 1) & 1], &ctl->dcount[g - 1]};
+        SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1)};
         launch_snapshot(sa, grid_k, s);
         c->launches++;
       }
@@ -594,6 +595,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       ma.hnext = c->hnext;
       ma.head = c->head;
       ma.hmask = c->hcap - 1;
+      ma.worklist = use_work ? (const int32_t *)c->work.p : nullptr;
+      ma.nwork = &ctl->nwork[st];
       ma.deg = c->deg;
       ma.deg_total = &ctl->deg_total;
       ma.candT = c->candT;
@@ -612,7 +615,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     }
     if (st == 0 && mask != RAPID_MASK_OFF) {
       Timer tm(c, s, RAPID_K_PREDICT, st);
-      SnapArgs sa{sp, K, nullptr, nullptr};
+      SnapArgs sa{sp, K, 0u};
       launch_snapshot(sa, grid_k, s);
       c->launches++;
       PredictArgs pr;
@@ -645,6 +648,9 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     fa.byp = T + P.o_byp;
     fa.remap_pending = &ctl->remap_pending[nst - 1];
     fa.labels = labels;
+    const bool last_work = nst > 1 && tile_gate;
+    fa.worklist = last_work ? (const int32_t *)c->work.p : nullptr;
+    fa.nwork = &ctl->nwork[nst - 1];
     launch_final(fa, P.st[nst - 1].b > 1, s);
     c->launches++;
   }
@@ -678,7 +684,7 @@ void rapid_free(rapid_ctx *c) {
   cudaGetDevice(&prev);
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  void *ptrs[] = {c->sums, c->rc, c->rec, c->init, c->out, c->remap, c->dl[0], c->dl[1], c->head,
+  void *ptrs[] = {c->sums, c->rc, c->rec, c->init, c->out, c->remap, c->head,
                   c->vlist, c->alist, c->pairs, c->alive, c->active, c->victim, c->y, c->dirty,
                   c->deg, c->chunk, c->hkeys, c->candE, c->hvals, c->hnext, c->candT, c->ctl,
                   c->candV, c->mlock, c->res,
@@ -712,7 +718,7 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   c->hcap = hc;
   if ((rc = dalloc(c, &c->sums, K * SUMW)) || (rc = dalloc(c, &c->rc, K * SUMW)) ||
       (rc = dalloc(c, &c->rec, K)) || (rc = dalloc(c, &c->init, K)) || (rc = dalloc(c, &c->out, K)) ||
-      (rc = dalloc(c, &c->remap, K)) || (rc = dalloc(c, &c->dl[0], K)) || (rc = dalloc(c, &c->dl[1], K)) ||
+      (rc = dalloc(c, &c->remap, K)) ||
       (rc = dalloc(c, &c->head, K)) || (rc = dalloc(c, &c->vlist, K)) || (rc = dalloc(c, &c->alist, K)) ||
       (rc = dalloc(c, &c->pairs, 2 * K)) || (rc = dalloc(c, &c->alive, K)) ||
       (rc = dalloc(c, &c->active, K)) || (rc = dalloc(c, &c->victim, K)) || (rc = dalloc(c, &c->y, K)) ||

@@ -32,9 +32,28 @@ struct __align__(16) Rec {
 constexpr uint32_t F_ALIVE = 1u, F_ACTIVE = 2u;
 // y is stored as (y + 1) in bits 2..3
 
+// Division by a runtime-constant divisor d >= 1 for n < 2^31: with s = ceil(log2 d) and
+// m = ceil(2^(31+s) / d) (< 2^32), floor(n/d) = umulhi(n, m) >> (s-1)  (error n*e < 2^(31+s)).
+struct FastDiv {
+  uint32_t d, m, s;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0, 0};
+  if (d <= 1) return f;
+  uint32_t s = 0;
+  while ((1ull << s) < d) s++;
+  f.m = (uint32_t)(((1ull << (31 + s)) + d - 1) / d);
+  f.s = s - 1;
+  return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
+  return f.d <= 1 ? n : (__umulhi(n, f.m) >> f.s);
+}
+
 struct StageDev {
   int32_t nbx, nby, b;
   int32_t tiles_x, tiles_y;      // sweep tiles per image
+  FastDiv fd_tx, fd_ty;          // division by tiles_x / tiles_y
   const int32_t *xs, *ys;        // block boundaries (nbx+1, nby+1)
   const int32_t *px, *py;        // parent block index in stage s-1 (s > 0)
   const int32_t *cxs, *cys;      // first child index in stage s+1 (nbx+1, nby+1)
@@ -102,49 +121,35 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 // Warp-aggregated delta update of the six int64 sums of superpixel `key` (north star (d)):
-// lanes with the same key are reduced with shuffles and one lane issues the atomics.
-// Integer atomics are order-independent, so the result is deterministic.
+// __match_any_sync groups the lanes by key, every group is reduced at once with REDUX
+// (__reduce_add_sync on 16-bit halves: each d[f] is in [0, 2^47), so no 32-bit partial sum
+// overflows), and each group's leader issues fire-and-forget int64 atomics.  Integer
+// atomics are order-independent, so the result is deterministic.  The leader also stamps the
+// superpixel dirty (the next snapshot refreshes stamped records only).
+// Must be called by all 32 lanes (uniform control flow).
 __device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[6], bool negate,
-                                         unsigned long long *sums, uint32_t *dirty, uint32_t stamp,
-                                         int32_t *dlist, unsigned int *dcount) {
-  unsigned pend = __ballot_sync(FULL, valid);
-  const int lane = lane_id();
-  while (pend) {
-    const int src = __ffs(pend) - 1;
-    const int k = __shfl_sync(FULL, key, src);
-    const bool in = valid && key == k;
-    const unsigned grp = __ballot_sync(FULL, in);
+                                         unsigned long long *sums, uint32_t *dirty, uint32_t stamp) {
+  const unsigned act = __ballot_sync(FULL, valid);
+  if (!valid) return;
+  const unsigned grp = __match_any_sync(act, key);
+  const bool leader = lane_id() == __ffs(grp) - 1;
 #pragma unroll
-    for (int f = 0; f < 6; f++) {
-      long long v = in ? d[f] : 0;
-      v = warp_sum_ll(v);
-      if (lane == src) atomicAdd(&sums[(size_t)k * SUMW + f], (unsigned long long)(negate ? -v : v));
-    }
-    if (lane == src && dirty != nullptr) {
-      if (atomicExch(&dirty[k], stamp) != stamp) {
-        unsigned pos = atomicAdd(dcount, 1u);
-        dlist[pos] = k;
-      }
-    }
-    pend &= ~grp;
+  for (int f = 0; f < 6; f++) {
+    const unsigned lo = __reduce_add_sync(grp, (unsigned)(d[f] & 0xffff));
+    const unsigned hi = __reduce_add_sync(grp, (unsigned)(d[f] >> 16));
+    const long long tot = ((long long)hi << 16) + (long long)lo;
+    if (leader) atomicAdd(&sums[(size_t)key * SUMW + f], (unsigned long long)(negate ? -tot : tot));
   }
+  if (leader && dirty != nullptr) dirty[key] = stamp;
 }
 
-// Warp-aggregated int32 add (proposal outflow per source superpixel).
+// Warp-aggregated int32 add (proposal outflow per source superpixel); v in [0, 2^16).
 __device__ __forceinline__ void agg_add_i32(bool valid, int key, int v, int32_t *arr) {
-  unsigned pend = __ballot_sync(FULL, valid);
-  const int lane = lane_id();
-  while (pend) {
-    const int src = __ffs(pend) - 1;
-    const int k = __shfl_sync(FULL, key, src);
-    const bool in = valid && key == k;
-    const unsigned grp = __ballot_sync(FULL, in);
-    int s = in ? v : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
-    if (lane == src) atomicAdd(&arr[k], s);
-    pend &= ~grp;
-  }
+  const unsigned act = __ballot_sync(FULL, valid);
+  if (!valid) return;
+  const unsigned grp = __match_any_sync(act, key);
+  const unsigned s = __reduce_add_sync(grp, (unsigned)v);
+  if (lane_id() == __ffs(grp) - 1) atomicAdd(&arr[key], (int)s);
 }
 
 // Block data of a block at stage `st`: n, colour sums, position sums (x = column).

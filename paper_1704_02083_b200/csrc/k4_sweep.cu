@@ -32,7 +32,7 @@ typedef __int128 i128;
 constexpr int HX = 4;
 constexpr int BOXW = TX + 2 * HX;  // 72 int32 = 288 B
 constexpr int BOXH = TY + 2;       // 18
-constexpr int NSTAGE = 4;
+constexpr int NSTAGE = 6;
 constexpr unsigned TILE_BYTES = BOXH * BOXW * 4;
 constexpr int STAGE_INTS = (BOXH * BOXW + 31) / 32 * 32;  // each TMA destination 128-B aligned
 
@@ -202,8 +202,8 @@ __device__ __forceinline__ void eval_warp(const PhaseArgs &a, const QE *q, int n
     const size_t idx = ((size_t)img * nby + gy) * nbx + gx;
     if (!GATED) {  // size_mode NONE: no budget to check, commit in place
       if (prop) a.st.map[idx] = Bm;
-      agg_sums(prop, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp, a.dlist, a.dcount);
-      agg_sums(prop, kb + Bm, d, false, a.sp.sums, a.sp.dirty, a.stamp, a.dlist, a.dcount);
+      agg_sums(prop, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp);
+      agg_sums(prop, kb + Bm, d, false, a.sp.sums, a.sp.dirty, a.stamp);
       c.commit += __popc(pm);
     } else {
       agg_add_i32(prop, kb + A, (int)d[0], a.sp.out);
@@ -294,7 +294,8 @@ __global__ void __launch_bounds__(K4_THREADS, K4_MIN_BLOCKS) k_sweep(const Phase
   __shared__ __align__(8) uint64_t full[NSTAGE], empty[NSTAGE];
   __shared__ int4 s_info[NSTAGE];  // gx0, gy0, img, border
   __shared__ __align__(16) QE q[NWARP][WQCAP];
-  __shared__ __align__(16) int32_t wrow[NWARP][3][BOXW];  // LDG loader: private rows
+  // LDG loader: private 3-row windows per warp, carved from the (then unused) TMA ring
+  int32_t(*wrow)[3][BOXW] = reinterpret_cast<int32_t(*)[3][BOXW]>(&buf[0][0]);
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int nbx = a.st.nbx, nby = a.st.nby;
   const int tiles_x = a.st.tiles_x, tiles_y = a.st.tiles_y;
@@ -309,22 +310,36 @@ __global__ void __launch_bounds__(K4_THREADS, K4_MIN_BLOCKS) k_sweep(const Phase
   }
   __syncthreads();
 
-  if (warp == NWARP) {  // ---- producer
-    if (!USE_TMA || lane != 0) return;
-    for (unsigned k = 0;; k++) {
-      const unsigned w = blockIdx.x + k * gridDim.x;
-      if (w >= ntiles) break;
-      const int st = (int)(k % NSTAGE);
-      if (k >= NSTAGE) mbar_wait(&empty[st], ((k / NSTAGE) - 1) & 1u);
-      const int t = a.worklist ? a.worklist[w] : (int)w;
-      const int tx = t % tiles_x, r = t / tiles_x;
-      const int ty = r % tiles_y, img = r / tiles_y;
-      const int gx0 = tx * TX, gy0 = ty * TY;
-      const int border = (gx0 == 0 || gy0 == 0 || gx0 + TX + 1 > nbx || gy0 + TY + 1 > nby) ? 1 : 0;
-      s_info[st] = make_int4(gx0, gy0, img, border);
-      fence_proxy_async();
-      mbar_expect_tx(&full[st], TILE_BYTES);
-      tma_load_3d(&buf[st][0], &tmap, gx0 - HX, gy0 - 1, img, &full[st]);
+  if (warp == NWARP) {  // ---- producer warp: 32 tiles decoded in parallel, lane 0 issues
+    if (!USE_TMA) return;
+    for (unsigned kb = 0; blockIdx.x + kb * gridDim.x < ntiles; kb += 32) {
+      const unsigned wl = blockIdx.x + (kb + lane) * gridDim.x;
+      int4 inf = make_int4(0, 0, 0, 0);
+      if (wl < ntiles) {
+        const uint32_t t = a.worklist ? (uint32_t)a.worklist[wl] : wl;
+        const uint32_t r = fdiv(t, a.st.fd_tx), img = fdiv(r, a.st.fd_ty);
+        const int gx0 = (int)(t - r * (uint32_t)tiles_x) * TX, gy0 = (int)(r - img * (uint32_t)tiles_y) * TY;
+        const int border = (gx0 == 0 || gy0 == 0 || gx0 + TX + 1 > nbx || gy0 + TY + 1 > nby) ? 1 : 0;
+        inf = make_int4(gx0, gy0, (int)img, border);
+      }
+      for (int j = 0; j < 32; j++) {
+        const unsigned k = kb + j;
+        if (blockIdx.x + k * gridDim.x >= ntiles) break;  // warp-uniform
+        int4 v;
+        v.x = __shfl_sync(FULL, inf.x, j);
+        v.y = __shfl_sync(FULL, inf.y, j);
+        v.z = __shfl_sync(FULL, inf.z, j);
+        v.w = __shfl_sync(FULL, inf.w, j);
+        if (lane == 0) {
+          const int st = (int)(k % NSTAGE);
+          if (k >= NSTAGE) mbar_wait(&empty[st], ((k / NSTAGE) - 1) & 1u);
+          s_info[st] = v;
+          fence_proxy_async();
+          mbar_expect_tx(&full[st], TILE_BYTES);
+          tma_load_3d(&buf[st][0], &tmap, v.x - HX, v.y - 1, v.z, &full[st]);
+        }
+        __syncwarp();
+      }
     }
     return;
   }
@@ -356,12 +371,11 @@ __global__ void __launch_bounds__(K4_THREADS, K4_MIN_BLOCKS) k_sweep(const Phase
       }
       T = reinterpret_cast<const int32_t(*)[BOXW]>(rows + (HX - 1));
     } else {
-      const int t = a.worklist ? a.worklist[w] : (int)w;
-      const int tx = t % tiles_x, r = t / tiles_x;
-      const int ty = r % tiles_y;
-      img = r / tiles_y;
-      gx0 = tx * TX;
-      gy0 = ty * TY;
+      const uint32_t t = a.worklist ? (uint32_t)a.worklist[w] : w;
+      const uint32_t r = fdiv(t, a.st.fd_tx), im = fdiv(r, a.st.fd_ty);
+      img = (int)im;
+      gx0 = (int)(t - r * (uint32_t)tiles_x) * TX;
+      gy0 = (int)(r - im * (uint32_t)tiles_y) * TY;
       const int32_t *map = a.st.map + (size_t)img * nby * nbx;
       __syncwarp();
       int32_t v[(3 * BOXW + 31) / 32];
@@ -437,8 +451,8 @@ __global__ void __launch_bounds__(256) k_commit(const PhaseArgs a) {
         }
       }
     }
-    agg_sums(ok, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp, a.dlist, a.dcount);
-    agg_sums(ok, kb + B, d, false, a.sp.sums, a.sp.dirty, a.stamp, a.dlist, a.dcount);
+    agg_sums(ok, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp);
+    agg_sums(ok, kb + B, d, false, a.sp.sums, a.sp.dirty, a.stamp);
     c_commit += __popc(__ballot_sync(FULL, ok));
     c_rej += __popc(__ballot_sync(FULL, rej));
   }

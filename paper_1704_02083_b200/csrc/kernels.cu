@@ -108,7 +108,7 @@ __global__ void k_stats0(const InitArgs a) {
       else block_data_blk(st, img, gx, gy, d);
       key = img * a.M + st.map[t];
     }
-    agg_sums(valid, key, d, false, a.sp.sums, nullptr, 0, nullptr, nullptr);
+    agg_sums(valid, key, d, false, a.sp.sums, nullptr, 0);
   }
 }
 
@@ -141,9 +141,9 @@ __device__ __forceinline__ void make_rec(const SpDev &sp, int k) {
 }
 
 __global__ void k_snapshot(const SnapArgs a) {
-  const int n = a.list ? (int)*a.count : a.K;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    make_rec(a.sp, a.list ? a.list[i] : i);
+  // full refresh (stamp 0) or only the superpixels stamped dirty by the previous phase
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.K; i += gridDim.x * blockDim.x)
+    if (a.stamp == 0u || a.sp.dirty[i] == a.stamp) make_rec(a.sp, i);
 }
 
 
@@ -272,36 +272,37 @@ __global__ void k_merge_heads(const MergeArgs a) {
     a.head[a.vlist[i]] = -1;
 }
 
-// O7 step 1: (victim, neighbour) -> shared edge length over unordered 4-adjacent block pairs
+// O7 step 1: (victim, neighbour) -> shared edge length.  Counted from the victim's side: each
+// block p of a victim V adds, for every 4-neighbour q with L_q != V, the shared edge length
+// to len[V][L_q] — the same totals as summing over unordered adjacent pairs.  At gated
+// stages only worklist tiles can hold victim blocks (victims are active superpixels, and
+// active superpixels' blocks never leave the worklist tiles), so only those are scanned.
 __global__ void k_merge_adjacency(const MergeArgs a) {
   if (*a.victim_any == 0u) return;
   const StageDev &st = a.st;
-  const size_t nper = (size_t)st.nbx * st.nby;
-  const size_t n = nper * a.B;
+  const unsigned ntiles = a.worklist ? *a.nwork : (unsigned)(st.tiles_x * st.tiles_y) * (unsigned)a.B;
+  const size_t n = (size_t)ntiles * (TX * TY);
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
        t += (size_t)gridDim.x * blockDim.x) {
-    const int img = (int)(t / nper);
-    const size_t r = t - (size_t)img * nper;
-    const int gy = (int)(r / st.nbx), gx = (int)(r - (size_t)gy * st.nbx);
-    const int kb = img * a.M;
-    const int la = st.map[t];
-    const bool va = a.sp.victim[kb + la] != 0;
-    if (gx + 1 < st.nbx) {
-      const int lb = st.map[t + 1];
-      if (lb != la) {
-        const unsigned e = (unsigned)(st.ys[gy + 1] - st.ys[gy]);
-        if (va) hash_add(a, kb + la, kb + lb, e);
-        if (a.sp.victim[kb + lb]) hash_add(a, kb + lb, kb + la, e);
-      }
-    }
-    if (gy + 1 < st.nby) {
-      const int lb = st.map[t + st.nbx];
-      if (lb != la) {
-        const unsigned e = (unsigned)(st.xs[gx + 1] - st.xs[gx]);
-        if (va) hash_add(a, kb + la, kb + lb, e);
-        if (a.sp.victim[kb + lb]) hash_add(a, kb + lb, kb + la, e);
-      }
-    }
+    const unsigned w = (unsigned)(t / (TX * TY));
+    const int off = (int)(t - (size_t)w * (TX * TY));
+    const uint32_t tile = a.worklist ? (uint32_t)a.worklist[w] : w;
+    const uint32_t r = fdiv(tile, st.fd_tx), img = fdiv(r, st.fd_ty);
+    const int gx = (int)(tile - r * (uint32_t)st.tiles_x) * TX + (off % TX);
+    const int gy = (int)(r - img * (uint32_t)st.tiles_y) * TY + (off / TX);
+    if (gx >= st.nbx || gy >= st.nby) continue;
+    const int32_t *map = st.map + (size_t)img * st.nby * st.nbx;
+    const size_t p = (size_t)gy * st.nbx + gx;
+    const int la = map[p];
+    const int nq[4] = {gy > 0 ? map[p - st.nbx] : la, gx + 1 < st.nbx ? map[p + 1] : la,
+                       gy + 1 < st.nby ? map[p + st.nbx] : la, gx > 0 ? map[p - 1] : la};
+    if (nq[0] == la && nq[1] == la && nq[2] == la && nq[3] == la) continue;
+    const int kb = (int)img * a.M;
+    if (!a.sp.victim[kb + la]) continue;
+    const unsigned ew = (unsigned)(st.xs[gx + 1] - st.xs[gx]), eh = (unsigned)(st.ys[gy + 1] - st.ys[gy]);
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+      if (nq[q] != la) hash_add(a, kb + la, kb + nq[q], (q & 1) ? eh : ew);
   }
 }
 
@@ -625,7 +626,7 @@ __global__ void k_recount(const RecountArgs a) {
       else block_data_blk(st, img, gx, gy, d);
       key = img * a.M + st.map[t];
     }
-    agg_sums(valid, key, d, false, a.rc, nullptr, 0, nullptr, nullptr);
+    agg_sums(valid, key, d, false, a.rc, nullptr, 0);
   }
 }
 
@@ -656,14 +657,24 @@ __global__ void k_final_upsample(const FinalArgs a) {
 }
 
 __global__ void k_final_remap(const FinalArgs a) {
+  // in place on the map of `last` (== labels); merged-away labels only occur in worklist
+  // tiles at gated stages (victims are active superpixels)
   if (*a.remap_pending == 0u) return;
-  const size_t nper = (size_t)a.H * a.W;
-  const size_t n = nper * a.B;
+  const StageDev &st = a.last;
+  const unsigned ntiles = a.worklist ? *a.nwork : (unsigned)(st.tiles_x * st.tiles_y) * (unsigned)a.B;
+  const size_t n = (size_t)ntiles * (TX * TY);
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
        t += (size_t)gridDim.x * blockDim.x) {
-    const int img = (int)(t / nper);
-    const int l = a.labels[t];
-    if (!a.sp.alive[img * a.M + l]) a.labels[t] = a.sp.remap[img * a.M + l];
+    const unsigned w = (unsigned)(t / (TX * TY));
+    const int off = (int)(t - (size_t)w * (TX * TY));
+    const uint32_t tile = a.worklist ? (uint32_t)a.worklist[w] : w;
+    const uint32_t r = fdiv(tile, st.fd_tx), img = fdiv(r, st.fd_ty);
+    const int gx = (int)(tile - r * (uint32_t)st.tiles_x) * TX + (off % TX);
+    const int gy = (int)(r - img * (uint32_t)st.tiles_y) * TY + (off / TX);
+    if (gx >= st.nbx || gy >= st.nby) continue;
+    const size_t p = ((size_t)img * st.nby + gy) * st.nbx + gx;
+    const int l = a.labels[p];
+    if (!a.sp.alive[img * a.M + l]) a.labels[p] = a.sp.remap[img * a.M + l];
   }
 }
 

@@ -19,9 +19,7 @@ struct PhaseArgs {
   const unsigned int *nwork; // device count of the worklist
   uint4 *props;              // proposals {stage-map index, A, B, packed RGB (pixel stage)}
   unsigned long long *prop_count;
-  int32_t *dlist;            // dirty list of this phase
-  unsigned int *dcount;
-  uint32_t stamp;
+  uint32_t stamp;            // dirty stamp of this phase (superpixels whose sums change)
   unsigned long long *cnt;        // [NCNT] counters of this phase
   const unsigned long long *prev; // counters of the previous sweep (phase 0), or null
   uint32_t *victim_any;
@@ -30,8 +28,7 @@ struct PhaseArgs {
 struct SnapArgs {
   SpDev sp;
   int32_t K;
-  const int32_t *list;        // dirty list (null: all K)
-  const unsigned int *count;
+  uint32_t stamp;             // 0: refresh all; else only superpixels with dirty == stamp
 };
 
 struct MergeArgs {
@@ -52,6 +49,8 @@ struct MergeArgs {
   int32_t *hnext;
   int32_t *head;             // [K]
   unsigned long long hmask;
+  const int32_t *worklist;   // active tiles of this stage (null: every tile)
+  const unsigned int *nwork;
   // candidates
   unsigned int *deg;         // [victims] -> offsets (in place scan)
   unsigned int *deg_total;
@@ -114,6 +113,8 @@ struct FinalArgs {
   const int32_t *bxp, *byp;  // block column / row of each pixel column / row
   const uint32_t *remap_pending;
   int32_t *labels;           // [B][H][W]
+  const int32_t *worklist;   // remap pass: active tiles of `last` (null: every tile)
+  const unsigned int *nwork;
 };
 
 // launch wrappers (all enqueue on `s`)

@@ -19,6 +19,7 @@ namespace {
 struct Ctl {  // per-segmentation device control block (zeroed at the start of each call)
   unsigned long long cnt[MAXS][MAXSW][4][NCNT];
   unsigned long long prop_count[MAXS * MAXSW * 4];
+  unsigned long long cand_count[MAXS * MAXSW * 4];
   unsigned long long stage_info[MAXS][4];
   unsigned int victim_any[MAXS];
   unsigned int remap_pending[MAXS];
@@ -90,11 +91,11 @@ struct rapid_ctx {
   uint32_t *mlock = nullptr, *res = nullptr;
   Ctl *ctl = nullptr;
   // plan-sized buffers
-  DevBuf tab, bsum, maps[2], props, work;
+  DevBuf tab, bsum, maps[2], props, work, cands;
   // host-API staging
   DevBuf himg, hlab;
   // occupancy
-  int prop_grid[2][2] = {{0, 0}, {0, 0}};
+  int scan_grid = 0, eval_grid = 0;  // persistent grid sizes (CTAs)
   bool use_tma = true;  // RAPID_NO_TMA=1 forces the LDG tile loader (A/B testing)
   // profiling
   int prof = 0;  // 0 off, 1 events, 2 events + window counting
@@ -332,6 +333,10 @@ int build_plan(rapid_ctx *c, int H, int W, const rapid_params *p) {
   if ((rc = ensure(c, c->maps[0], N.map_max * 4))) return rc;
   if ((rc = ensure(c, c->maps[1], N.map_max * 4))) return rc;
   if ((rc = ensure(c, c->props, N.props_max * 16))) return rc;
+  // candidate list: every block of a phase colour may be a candidate, plus the chunked
+  // reservation slack of every scanning warp
+  const size_t cand_max = N.props_max + (size_t)c->scan_grid * 8 * CAND_SLACK_PER_WARP;
+  if ((rc = ensure(c, c->cands, cand_max * 32))) return rc;
   if ((rc = ensure(c, c->work, N.tiles_max * 4))) return rc;
   cudaError_t e = cudaMemcpy(c->tab.p, N.tab.data(), N.tab.size() * 4, cudaMemcpyHostToDevice);
   if ((rc = cuda_check(c, e, "upload tables"))) return rc;
@@ -547,6 +552,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           pa.worklist = use_work ? (const int32_t *)c->work.p : nullptr;
           pa.nwork = &ctl->nwork[st];
           pa.props = (uint4 *)c->props.p;
+          pa.cands = (uint4 *)c->cands.p;
+          pa.cand_count = &ctl->cand_count[g];
           pa.prop_count = &ctl->prop_count[g];
           pa.stamp = c->stamp_base + (uint32_t)g;
           pa.cnt = &ctl->cnt[st][t][ph][0];
@@ -555,8 +562,9 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           if (gated_sz) cudaMemsetAsync(c->out, 0, sizeof(int32_t) * K, s);
           {
             Timer t2(c, s, RAPID_K_PROPOSE, st);
-            launch_propose(pa, has_tmap[st] ? tmaps[st].b : nullptr, pixel,
-                           c->sm_count * c->prop_grid[pixel][gated_sz], s);
+            launch_scan(pa, has_tmap[st] ? tmaps[st].b : nullptr, c->scan_grid, s);
+            launch_eval(pa, pixel, c->eval_grid, s);
+            c->launches++;
             c->launches++;
           }
           if (gated_sz) {
@@ -688,7 +696,7 @@ void rapid_free(rapid_ctx *c) {
                   c->vlist, c->alist, c->pairs, c->alive, c->active, c->victim, c->y, c->dirty,
                   c->deg, c->chunk, c->hkeys, c->candE, c->hvals, c->hnext, c->candT, c->ctl,
                   c->candV, c->mlock, c->res,
-                  c->tab.p, c->bsum.p, c->maps[0].p, c->maps[1].p, c->props.p, c->work.p,
+                  c->tab.p, c->bsum.p, c->maps[0].p, c->maps[1].p, c->props.p, c->work.p, c->cands.p,
                   c->himg.p, c->hlab.p};
   for (void *q : ptrs)
     if (q) cudaFree(q);
@@ -737,8 +745,8 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   cudaMemset(c->mlock, 0, K * 4);
   cudaMemset(c->res, 0xff, K * 4);
   cudaMemset(c->rc, 0, K * SUMW * 8);
-  for (int px = 0; px < 2; px++)
-    for (int gs = 0; gs < 2; gs++) c->prop_grid[px][gs] = propose_occupancy(px, gs);
+  c->scan_grid = c->sm_count * scan_occupancy();
+  c->eval_grid = c->sm_count * eval_occupancy();
   {
     const char *e = getenv("RAPID_NO_TMA");
     c->use_tma = !(e && e[0] == '1');

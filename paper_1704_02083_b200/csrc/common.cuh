@@ -127,29 +127,65 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 // atomics are order-independent, so the result is deterministic.  The leader also stamps the
 // superpixel dirty (the next snapshot refreshes stamped records only).
 // Must be called by all 32 lanes (uniform control flow).
+// Runs of adjacent lanes with equal keys (invalid lanes get unique keys): run start of this
+// lane and whether it ends its run.  Full-mask intrinsics only (a per-group mask makes the
+// compiler emit a divergent slow path).
+struct WarpRun {
+  int start;
+  bool end;
+};
+__device__ __forceinline__ WarpRun warp_runs(bool valid, int key) {
+  const int lane = lane_id();
+  const int k = valid ? key : -1 - lane;
+  const int kp = __shfl_up_sync(FULL, k, 1);
+  const bool st = lane == 0 || kp != k;
+  const unsigned sm = __ballot_sync(FULL, st);
+  WarpRun r;
+  r.start = 31 - __clz(sm & ((2u << lane) - 1u));
+  r.end = lane == 31 || ((sm >> (lane + 1)) & 1u);
+  return r;
+}
+
 __device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[6], bool negate,
                                          unsigned long long *sums, uint32_t *dirty, uint32_t stamp) {
-  const unsigned act = __ballot_sync(FULL, valid);
-  if (!valid) return;
-  const unsigned grp = __match_any_sync(act, key);
-  const bool leader = lane_id() == __ffs(grp) - 1;
+  if (__ballot_sync(FULL, valid) == 0u) return;  // warp-uniform
+  const WarpRun run = warp_runs(valid, key);
+  const int lane = lane_id();
+  // segmented inclusive scan over each run: n, r, g, b fit 32 bits (block <= 64^2 pixels),
+  // position sums need 64 bits
+  unsigned v0 = valid ? (unsigned)d[0] : 0u, v1 = valid ? (unsigned)d[1] : 0u;
+  unsigned v2 = valid ? (unsigned)d[2] : 0u, v3 = valid ? (unsigned)d[3] : 0u;
+  long long v4 = valid ? d[4] : 0, v5 = valid ? d[5] : 0;
 #pragma unroll
-  for (int f = 0; f < 6; f++) {
-    const unsigned lo = __reduce_add_sync(grp, (unsigned)(d[f] & 0xffff));
-    const unsigned hi = __reduce_add_sync(grp, (unsigned)(d[f] >> 16));
-    const long long tot = ((long long)hi << 16) + (long long)lo;
-    if (leader) atomicAdd(&sums[(size_t)key * SUMW + f], (unsigned long long)(negate ? -tot : tot));
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned t0 = __shfl_up_sync(FULL, v0, o), t1 = __shfl_up_sync(FULL, v1, o);
+    const unsigned t2 = __shfl_up_sync(FULL, v2, o), t3 = __shfl_up_sync(FULL, v3, o);
+    const long long t4 = __shfl_up_sync(FULL, v4, o), t5 = __shfl_up_sync(FULL, v5, o);
+    if (lane - o >= run.start) {
+      v0 += t0; v1 += t1; v2 += t2; v3 += t3; v4 += t4; v5 += t5;
+    }
   }
-  if (leader && dirty != nullptr) dirty[key] = stamp;
+  if (valid && run.end) {
+    const long long tot[6] = {(long long)v0, (long long)v1, (long long)v2, (long long)v3, v4, v5};
+    unsigned long long *s = sums + (size_t)key * SUMW;
+#pragma unroll
+    for (int f = 0; f < 6; f++) atomicAdd(&s[f], (unsigned long long)(negate ? -tot[f] : tot[f]));
+    if (dirty != nullptr) dirty[key] = stamp;
+  }
 }
 
 // Warp-aggregated int32 add (proposal outflow per source superpixel); v in [0, 2^16).
 __device__ __forceinline__ void agg_add_i32(bool valid, int key, int v, int32_t *arr) {
-  const unsigned act = __ballot_sync(FULL, valid);
-  if (!valid) return;
-  const unsigned grp = __match_any_sync(act, key);
-  const unsigned s = __reduce_add_sync(grp, (unsigned)v);
-  if (lane_id() == __ffs(grp) - 1) atomicAdd(&arr[key], (int)s);
+  if (__ballot_sync(FULL, valid) == 0u) return;  // warp-uniform
+  const WarpRun run = warp_runs(valid, key);
+  const int lane = lane_id();
+  int s = valid ? v : 0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(FULL, s, o);
+    if (lane - o >= run.start) s += t;
+  }
+  if (valid && run.end) atomicAdd(&arr[key], s);
 }
 
 // Block data of a block at stage `st`: n, colour sums, position sums (x = column).

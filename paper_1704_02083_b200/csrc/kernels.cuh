@@ -17,6 +17,8 @@ struct PhaseArgs {
   long long lam_pos, lam_b;  // Q16
   const int32_t *worklist;   // null: every tile of the stage
   const unsigned int *nwork; // device count of the worklist
+  uint4 *cands;              // K4a -> K4b candidate list (2 x uint4 per entry)
+  unsigned long long *cand_count;
   uint4 *props;              // proposals {stage-map index, A, B, packed RGB (pixel stage)}
   unsigned long long *prop_count;
   uint32_t stamp;            // dirty stamp of this phase (superpixels whose sums change)
@@ -126,9 +128,13 @@ void launch_pyramid_up(const StageDev &parent, const StageDev &child, int B, uin
 void launch_init_map0(const InitArgs &a, cudaStream_t s);
 void launch_stats0(const InitArgs &a, cudaStream_t s);
 void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s);
-// K4: tmap = TMA descriptor of the stage map (CUtensorMap*), or null for the LDG loader
-void launch_propose(const PhaseArgs &a, const void *tmap, bool pixel, int grid, cudaStream_t s);
+// K4a: tmap = TMA descriptor of the stage map (CUtensorMap*), or null for the LDG loader
+void launch_scan(const PhaseArgs &a, const void *tmap, int grid, cudaStream_t s);
+void launch_eval(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
 void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
+int scan_occupancy();
+int eval_occupancy();
+constexpr int CAND_SLACK_PER_WARP = 64;  // chunked reservations: unused tail per scanning warp
 // encode a 3-D TMA descriptor {nbx, nby, B} of int32 with box {TX+4, TY+2, 1};
 // false when nbx*4 is not a multiple of 16 B (the LDG loader is used then)
 bool make_label_tmap(void *tmap64B, int32_t *base, int nbx, int nby, int B);
@@ -137,7 +143,6 @@ void launch_predict(const PredictArgs &a, int grid, cudaStream_t s, int *nlaunch
 void launch_transition(const TransArgs &a, cudaStream_t s);
 void launch_recount(const RecountArgs &a, bool pixel, int grid, cudaStream_t s, int *nlaunch);
 void launch_final(const FinalArgs &a, bool upsample, cudaStream_t s);
-int propose_occupancy(bool pixel, bool gated);
 void launch_count_window(const StageDev &st, const SpDev &sp, int B, int M, unsigned long long *out,
                          cudaStream_t s);
 

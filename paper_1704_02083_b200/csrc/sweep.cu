@@ -1,0 +1,505 @@
+// sweep.cu — the parity-phase boundary sweep on sm_100a: K4a scan, K4b evaluate, K5 commit.
+//
+// One phase c = (cx, cy) of one sweep (DESIGN §2 A5/A6) tests every block of colour c of the
+// stage map in parallel against frozen per-phase means (A4):
+//   boundary (Eq. 2) -> gate (Eq. 7 / prediction) -> simple point (E_topo)
+//   -> Eq. 3 argmin over the distinct 4-neighbour labels of the Eq. 1 energy difference
+//   -> size gate (E_size P:68 / RAPID l.19) -> commit or proposal.
+//
+// K4a  k_scan (streaming, HBM-bound): persistent warp-specialised CTAs over the tile
+//      worklist.  A producer lane streams (TY+2) x (TX+8) label tiles (1-block halo,
+//      16-B aligned box) with TMA (cp.async.bulk.tensor.3d) into an NSTAGE shared-memory
+//      ring; full/empty mbarriers hand the stages to 8 consumer warps, one candidate row
+//      (32 blocks of the phase colour) each.  Consumers test boundary + 3x3 simple point in
+//      shared memory, gate the boundary blocks, and append the survivors — with their 4
+//      neighbour labels — to a compact global candidate list (per-warp chunk reservations).
+//      Maps whose row pitch is not a multiple of 16 B use a per-warp LDG loader.
+// K4b  k_eval (gather-bound, full occupancy): one candidate per thread — colour, 32-B
+//      snapshot records of A and its neighbours (L2), int64/int128 energy, argmin, size
+//      gate — then warp-aggregated int64 atomics (size_mode NONE: commit in place) or
+//      proposals (HARD/MERGE).
+// K5   k_commit: all-or-nothing size budget per source superpixel (A19), label writes,
+//      warp-aggregated stats deltas.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "kernels.cuh"
+
+namespace rapid {
+
+typedef __int128 i128;
+
+// The TMA box starts HX = 4 blocks left of the tile: the inner coordinate of a tile load
+// must be 16-B aligned (measured: x = -1 faults, x = -4 loads); width TX + 8 = 72 int32.
+constexpr int HX = 4;
+constexpr int BOXW = TX + 2 * HX;  // 72 int32 = 288 B
+constexpr int BOXH = TY + 2;       // 18
+constexpr int NSTAGE = 6;
+constexpr unsigned TILE_BYTES = BOXH * BOXW * 4;
+constexpr int STAGE_INTS = (BOXH * BOXW + 31) / 32 * 32;  // each TMA destination 128-B aligned
+constexpr int NWARP = TY / 2;                             // consumer warps (one candidate row each)
+constexpr int K4A_THREADS = (NWARP + 1) * 32;
+constexpr int CHUNK = 64;                                 // candidate slots reserved per atomic
+constexpr int K4B_THREADS = 256;
+
+// candidate entry (32 B = 2 x uint4): {pos = gx | gy << 16, img, A, N}, {E, S, W, 0};
+// A = -1 marks an unused reserved slot.
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *m, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *m) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *m, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(m)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z,
+                                            uint64_t *m) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(m))
+      : "memory");
+}
+
+// 2^(-16) x the oracle's weighted dE (same sign, same order): exact Eq. 1 difference of
+// relabelling a pixel set with data d from A to B under the frozen quantised means.
+__device__ __forceinline__ i128 delta_e(const RecV &ra, const RecV &rb, const long long d[6],
+                                        long long dB2, long long lam_pos, long long lam_b) {
+  const long long n = d[0];
+  const long long dC = (rb.c0 - ra.c0) * (n * (rb.c0 + ra.c0) - (d[1] << (FRAC + 1))) +
+                       (rb.c1 - ra.c1) * (n * (rb.c1 + ra.c1) - (d[2] << (FRAC + 1)));
+  const i128 dCw = (i128)dC + (i128)((rb.c2 - ra.c2) * (n * (rb.c2 + ra.c2) - (d[3] << (FRAC + 1))));
+  const long long dP = (rb.mx - ra.mx) * (n * (rb.mx + ra.mx) - (d[4] << (FRAC + 1))) +
+                       (rb.my - ra.my) * (n * (rb.my + ra.my) - (d[5] << (FRAC + 1)));
+  return (dCw << 16) + (i128)lam_pos * (i128)dP + ((i128)(lam_b * dB2) << 16);
+}
+
+// Work count of a list-driven kernel, read once per CTA (thread 0) and broadcast through
+// shared memory: 0 when the sweep is skipped (A25) or the list is empty, and also 0 for
+// CTAs whose first element lies beyond the list.  Must be called by all threads.
+__device__ __forceinline__ unsigned long long cta_count(const unsigned long long *prev,
+                                                         const unsigned long long *count) {
+  __shared__ unsigned long long s_n;
+  if (threadIdx.x == 0) s_n = sweep_skipped(prev) ? 0ull : *count;
+  __syncthreads();
+  const unsigned long long n = s_n;
+  return (unsigned long long)blockIdx.x * blockDim.x < n ? n : 0ull;
+}
+
+
+// ------------------------------------------------------------------ K4a: scan
+template <bool USE_TMA>
+__global__ void __launch_bounds__(K4A_THREADS) k_scan(const PhaseArgs a,
+                                                      const __grid_constant__ CUtensorMap tmap) {
+  if (sweep_skipped(a.prev)) return;
+  __shared__ __align__(128) int32_t buf[NSTAGE][STAGE_INTS];
+  __shared__ __align__(8) uint64_t full[NSTAGE], empty[NSTAGE];
+  __shared__ int4 s_info[NSTAGE];  // gx0, gy0, img, border
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int nbx = a.st.nbx, nby = a.st.nby;
+  const int tiles_x = a.st.tiles_x, tiles_y = a.st.tiles_y;
+  const unsigned ntiles = a.worklist ? *a.nwork : (unsigned)(tiles_x * tiles_y) * (unsigned)a.B;
+
+  if (threadIdx.x == 0 && USE_TMA) {
+    for (int s = 0; s < NSTAGE; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWARP);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == NWARP) {  // ---- producer warp: 32 tiles decoded in parallel, lane 0 issues
+    if (!USE_TMA) return;
+    for (unsigned kb = 0; blockIdx.x + kb * gridDim.x < ntiles; kb += 32) {
+      const unsigned wl = blockIdx.x + (kb + lane) * gridDim.x;
+      int4 inf = make_int4(0, 0, 0, 0);
+      if (wl < ntiles) {
+        const uint32_t t = a.worklist ? (uint32_t)a.worklist[wl] : wl;
+        const uint32_t r = fdiv(t, a.st.fd_tx), img = fdiv(r, a.st.fd_ty);
+        const int gx0 = (int)(t - r * (uint32_t)tiles_x) * TX, gy0 = (int)(r - img * (uint32_t)tiles_y) * TY;
+        const int border = (gx0 == 0 || gy0 == 0 || gx0 + TX + 1 > nbx || gy0 + TY + 1 > nby) ? 1 : 0;
+        inf = make_int4(gx0, gy0, (int)img, border);
+      }
+      for (int j = 0; j < 32; j++) {
+        const unsigned k = kb + j;
+        if (blockIdx.x + k * gridDim.x >= ntiles) break;  // warp-uniform
+        int4 v;
+        v.x = __shfl_sync(FULL, inf.x, j);
+        v.y = __shfl_sync(FULL, inf.y, j);
+        v.z = __shfl_sync(FULL, inf.z, j);
+        v.w = __shfl_sync(FULL, inf.w, j);
+        if (lane == 0) {
+          const int st = (int)(k % NSTAGE);
+          if (k >= NSTAGE) mbar_wait(&empty[st], ((k / NSTAGE) - 1) & 1u);
+          s_info[st] = v;
+          fence_proxy_async();
+          mbar_expect_tx(&full[st], TILE_BYTES);
+          tma_load_3d(&buf[st][0], &tmap, v.x - HX, v.y - 1, v.z, &full[st]);
+        }
+        __syncwarp();
+      }
+    }
+    return;
+  }
+
+  // ---- consumers
+  // LDG loader: private 3-row windows per warp, carved from the (then unused) TMA ring
+  int32_t(*wrow)[3][BOXW] = reinterpret_cast<int32_t(*)[3][BOXW]>(&buf[0][0]);
+  const int li = 2 * lane + a.cx;  // candidate column within the tile
+  const int lr = 2 * warp + a.cy;  // candidate row within the tile
+  unsigned c_cand = 0, c_topo = 0;
+  unsigned long long cbase = 0;
+  int cleft = 0;
+  for (unsigned k = 0;; k++) {
+    const unsigned w = blockIdx.x + k * gridDim.x;
+    if (w >= ntiles) break;
+    const int st = (int)(k % NSTAGE);
+    int gx0, gy0, img;
+    const int32_t(*T)[BOXW];
+    if (USE_TMA) {
+      mbar_wait(&full[st], (k / NSTAGE) & 1u);
+      const int4 inf = s_info[st];
+      gx0 = inf.x; gy0 = inf.y; img = inf.z;
+      int32_t *rows = buf[st] + lr * BOXW;  // smem rows lr .. lr+2 = gy-1 .. gy+1
+      if (inf.w) {  // TMA zero-fills outside the image; 0 is a label: mark "no block"
+        for (int idx = lane; idx < 3 * BOXW; idx += 32) {
+          const int r = idx / BOXW, cc = idx - r * BOXW;
+          const int y = gy0 + lr - 1 + r, x = gx0 + cc - HX;
+          if (x < 0 || x >= nbx || y < 0 || y >= nby) rows[idx] = -1;
+        }
+        __syncwarp();
+      }
+      T = reinterpret_cast<const int32_t(*)[BOXW]>(rows + (HX - 1));
+    } else {
+      const uint32_t t = a.worklist ? (uint32_t)a.worklist[w] : w;
+      const uint32_t r = fdiv(t, a.st.fd_tx), im = fdiv(r, a.st.fd_ty);
+      img = (int)im;
+      gx0 = (int)(t - r * (uint32_t)tiles_x) * TX;
+      gy0 = (int)(r - im * (uint32_t)tiles_y) * TY;
+      const int32_t *map = a.st.map + (size_t)img * nby * nbx;
+      __syncwarp();
+      constexpr int PER = (3 * BOXW + 31) / 32;
+      int32_t v[PER];
+#pragma unroll
+      for (int u = 0; u < PER; u++) {
+        const int idx = lane + 32 * u;
+        const int rr = idx / BOXW, cc = idx - rr * BOXW;
+        const int y = gy0 + lr - 1 + rr, x = gx0 + cc - HX;
+        v[u] = (idx < 3 * BOXW && x >= 0 && x < nbx && y >= 0 && y < nby) ? map[(size_t)y * nbx + x] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < PER; u++) {
+        const int idx = lane + 32 * u;
+        if (idx < 3 * BOXW) (&wrow[warp][0][0])[idx] = v[u];
+      }
+      __syncwarp();
+      T = reinterpret_cast<const int32_t(*)[BOXW]>(&wrow[warp][0][0] + (HX - 1));
+    }
+    // boundary (Eq. 2) + simple point (E_topo) from shared memory; T[r][c] = (gx0+c-1, gy-1+r)
+    const int gx = gx0 + li, gy = gy0 + lr;
+    bool bnd = false, topo_ok = false;
+    int A = -1, n0 = -1, n1 = -1, n2 = -1, n3 = -1;
+    if (gx < nbx && gy < nby) {
+      A = T[1][li + 1];
+      n0 = T[0][li + 1];  // N
+      n1 = T[1][li + 2];  // E
+      n2 = T[2][li + 1];  // S
+      n3 = T[1][li];      // W
+      bnd = (n0 >= 0 && n0 != A) | (n1 >= 0 && n1 != A) | (n2 >= 0 && n2 != A) | (n3 >= 0 && n3 != A);
+      if (bnd) {
+        const unsigned m = (unsigned)(n0 == A) | ((unsigned)(T[0][li + 2] == A) << 1) |
+                           ((unsigned)(n1 == A) << 2) | ((unsigned)(T[2][li + 2] == A) << 3) |
+                           ((unsigned)(n2 == A) << 4) | ((unsigned)(T[2][li] == A) << 5) |
+                           ((unsigned)(n3 == A) << 6) | ((unsigned)(T[0][li] == A) << 7);
+        topo_ok = simple_point(m);
+      }
+    }
+    __syncwarp();
+    if (USE_TMA && lane == 0) mbar_arrive(&empty[st]);  // tile slot free for the producer
+    // gate (A22): CLASS/BSP -> active[A]; EQ7 -> a neighbour of another label and class
+    bool cand = bnd;
+    if (bnd && a.gating) {
+      const int kb = img * a.M;
+      if (a.gating == 1) {
+        cand = a.sp.active[kb + A] != 0;
+      } else {
+        const int8_t yA = a.sp.y[kb + A];
+        cand = (n0 >= 0 && n0 != A && a.sp.y[kb + n0] != yA) || (n1 >= 0 && n1 != A && a.sp.y[kb + n1] != yA) ||
+               (n2 >= 0 && n2 != A && a.sp.y[kb + n2] != yA) || (n3 >= 0 && n3 != A && a.sp.y[kb + n3] != yA);
+      }
+    }
+    const bool emit = cand && topo_ok;
+    c_cand += __popc(__ballot_sync(FULL, cand));
+    const unsigned em = __ballot_sync(FULL, emit);
+    const int ne = __popc(em);
+    c_topo += ne;
+    if (ne) {
+      if (ne > cleft) {  // retire the rest of the chunk, reserve a new one
+        if (lane < cleft) a.cands[2 * (cbase + lane)] = make_uint4(0u, 0u, 0xffffffffu, 0u);
+        unsigned long long nb = 0;
+        if (lane == 0) nb = atomicAdd(a.cand_count, (unsigned long long)CHUNK);
+        cbase = __shfl_sync(FULL, nb, 0);
+        cleft = CHUNK;
+      }
+      if (emit) {
+        const unsigned long long slot = cbase + __popc(em & lanemask_lt());
+        a.cands[2 * slot] = make_uint4((uint32_t)gx | ((uint32_t)gy << 16), (uint32_t)img, (uint32_t)A, (uint32_t)n0);
+        a.cands[2 * slot + 1] = make_uint4((uint32_t)n1, (uint32_t)n2, (uint32_t)n3, 0u);
+      }
+      cbase += ne;
+      cleft -= ne;
+    }
+  }
+  if (lane < cleft) a.cands[2 * (cbase + lane)] = make_uint4(0u, 0u, 0xffffffffu, 0u);
+  if (cleft > 32 && lane + 32 < cleft) a.cands[2 * (cbase + lane + 32)] = make_uint4(0u, 0u, 0xffffffffu, 0u);
+  if (lane == 0) {
+    if (c_cand) atomicAdd(&a.cnt[0], (unsigned long long)c_cand);
+    if (c_topo) atomicAdd(&a.cnt[1], (unsigned long long)c_topo);
+  }
+}
+
+// ------------------------------------------------------------------ K4b: evaluate
+template <bool PIXEL, bool GATED>
+__global__ void __launch_bounds__(K4B_THREADS) k_eval(const PhaseArgs a) {
+  const unsigned long long n = cta_count(a.prev, a.cand_count);
+  if (n == 0) return;
+  const int lane = lane_id();
+  const int nbx = a.st.nbx, nby = a.st.nby;
+  unsigned c_prop = 0, c_srej = 0, c_commit = 0;
+  for (unsigned long long base = blockIdx.x * (unsigned long long)K4B_THREADS; base < n;
+       base += (unsigned long long)gridDim.x * K4B_THREADS) {  // warp-uniform trip count
+    const unsigned long long i = base + threadIdx.x;
+    bool prop = false, srej = false;
+    int A = 0, Bm = 0, kb = 0, gx = 0, gy = 0, img = 0;
+    uint32_t rgb = 0;
+    long long d[6] = {0, 0, 0, 0, 0, 0};
+    if (i < n) {
+      const uint4 e0 = a.cands[2 * i];
+      A = (int)e0.z;
+      if (A >= 0) {
+        const uint4 e1 = a.cands[2 * i + 1];
+        const int nq[4] = {(int)e0.w, (int)e1.x, (int)e1.y, (int)e1.z};
+        gx = (int)(e0.x & 0xffffu);
+        gy = (int)(e0.x >> 16);
+        img = (int)e0.y;
+        kb = img * a.M;
+        long long ew[4];
+        if (PIXEL) {
+          const uint8_t *p = a.image + (((size_t)img * a.H + gy) * a.W + gx) * 3;
+          const uint32_t r = p[0], g = p[1], b = p[2];
+          rgb = r | (g << 8) | (b << 16);
+          d[0] = 1; d[1] = r; d[2] = g; d[3] = b; d[4] = gx; d[5] = gy;
+          ew[0] = ew[1] = ew[2] = ew[3] = 1;
+        } else {
+          block_data_blk(a.st, img, gx, gy, d);
+          const long long bw = a.st.xs[gx + 1] - a.st.xs[gx], bh = a.st.ys[gy + 1] - a.st.ys[gy];
+          ew[0] = bw; ew[1] = bh; ew[2] = bw; ew[3] = bh;
+        }
+        // distinct candidate labels (A8), all record loads in flight together
+        int cb[4];
+        int nb = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const int B = nq[k];
+          bool u = B >= 0 && B != A;
+#pragma unroll
+          for (int r = 0; r < k; r++) u &= (nq[r] != B);
+          if (u) cb[nb++] = B;
+        }
+        const Rec recA = a.sp.rec[kb + A];
+        Rec rn[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          if (k < nb) rn[k] = a.sp.rec[kb + cb[k]];
+        const RecV ra = rec_vals(recA);
+        bool have = false;
+        i128 bestE = 0;
+        int bestB = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          if (k >= nb) break;
+          const int B = cb[k];
+          long long dB2 = 0;
+#pragma unroll
+          for (int r = 0; r < 4; r++)
+            if (nq[r] >= 0) dB2 += ew[r] * ((long long)(nq[r] != B) - (long long)(nq[r] != A));
+          const i128 E = delta_e(ra, rec_vals(rn[k]), d, 2 * dB2, a.lam_pos, a.lam_b);
+          if (!have || E < bestE || (E == bestE && B < bestB)) {
+            have = true;
+            bestE = E;
+            bestB = B;
+          }
+        }
+        if (have && bestE < 0) {
+          if (a.size_mode != 0 && ((long long)recA.n - d[0]) * a.l_den < a.l_num * (long long)recA.init) {
+            srej = true;  // A12: the desired move would leave A below l * InitSize
+            if (a.size_mode == 2) {
+              a.sp.victim[kb + A] = 1;
+              *a.victim_any = 1u;
+            }
+          } else {
+            prop = true;
+            Bm = bestB;
+          }
+        }
+      }
+    }
+    c_srej += __popc(__ballot_sync(FULL, srej));
+    const unsigned pm = __ballot_sync(FULL, prop);
+    c_prop += __popc(pm);
+    if (pm) {
+      const size_t idx = ((size_t)img * nby + gy) * nbx + gx;
+      if (!GATED) {  // size_mode NONE: no budget to check, commit in place
+        if (prop) a.st.map[idx] = Bm;
+        agg_sums(prop, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp);
+        agg_sums(prop, kb + Bm, d, false, a.sp.sums, a.sp.dirty, a.stamp);
+        c_commit += __popc(pm);
+      } else {
+        agg_add_i32(prop, kb + A, (int)d[0], a.sp.out);
+        unsigned long long pb = 0;
+        if (lane == 0) pb = atomicAdd(a.prop_count, (unsigned long long)__popc(pm));
+        pb = __shfl_sync(FULL, pb, 0);
+        if (prop)
+          a.props[pb + __popc(pm & lanemask_lt())] = make_uint4((unsigned)idx, (unsigned)A, (unsigned)Bm, rgb);
+      }
+    }
+  }
+  if (lane == 0) {
+    if (c_prop) atomicAdd(&a.cnt[2], (unsigned long long)c_prop);
+    if (c_srej) atomicAdd(&a.cnt[3], (unsigned long long)c_srej);
+    if (c_commit) atomicAdd(&a.cnt[4], (unsigned long long)c_commit);
+  }
+}
+
+// ------------------------------------------------------------------ K5: commit
+template <bool PIXEL>
+__global__ void __launch_bounds__(256) k_commit(const PhaseArgs a) {
+  const unsigned long long n = cta_count(a.prev, a.prop_count);
+  if (n == 0) return;
+  const size_t nper = (size_t)a.st.nbx * a.st.nby;
+  unsigned c_commit = 0, c_rej = 0;
+  for (unsigned long long base = blockIdx.x * 256ull; base < n; base += gridDim.x * 256ull) {
+    const unsigned long long i = base + threadIdx.x;
+    const bool valid = i < n;
+    bool ok = false, rej = false;
+    int A = 0, B = 0, kb = 0;
+    long long d[6] = {0, 0, 0, 0, 0, 0};
+    if (valid) {
+      const uint4 pr = a.props[i];
+      const size_t idx = pr.x;
+      A = (int)pr.y;
+      B = (int)pr.z;
+      const int img = (int)(idx / nper);
+      const size_t r = idx - (size_t)img * nper;
+      const int gy = (int)(r / a.st.nbx), gx = (int)(r - (size_t)gy * a.st.nbx);
+      kb = img * a.M;
+      const Rec ra = a.sp.rec[kb + A];
+      // O6' all-or-nothing budget: the total proposed outflow must keep A >= l * InitSize (A19)
+      ok = !(((long long)ra.n - (long long)a.sp.out[kb + A]) * a.l_den < a.l_num * (long long)ra.init);
+      if (ok) {
+        if (PIXEL) {
+          d[0] = 1; d[1] = pr.w & 0xffu; d[2] = (pr.w >> 8) & 0xffu; d[3] = (pr.w >> 16) & 0xffu;
+          d[4] = gx; d[5] = gy;
+        } else {
+          block_data_blk(a.st, img, gx, gy, d);
+        }
+        a.st.map[idx] = B;
+      } else {
+        rej = true;
+        if (a.size_mode == 2) {
+          a.sp.victim[kb + A] = 1;
+          *a.victim_any = 1u;
+        }
+      }
+    }
+    agg_sums(ok, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp);
+    agg_sums(ok, kb + B, d, false, a.sp.sums, a.sp.dirty, a.stamp);
+    c_commit += __popc(__ballot_sync(FULL, ok));
+    c_rej += __popc(__ballot_sync(FULL, rej));
+  }
+  if (lane_id() == 0) {
+    if (c_commit) atomicAdd(&a.cnt[4], (unsigned long long)c_commit);
+    if (c_rej) atomicAdd(&a.cnt[5], (unsigned long long)c_rej);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+bool make_label_tmap(void *tmap64B, int32_t *base, int nbx, int nby, int B) {
+  if (((size_t)nbx * 4) % 16 != 0) return false;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)nbx, (cuuint64_t)nby, (cuuint64_t)B};
+  const cuuint64_t strides[2] = {(cuuint64_t)nbx * 4, (cuuint64_t)nbx * nby * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)BOXW, (cuuint32_t)BOXH, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode((CUtensorMap *)tmap64B, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, base, dims, strides, box,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+
+int scan_occupancy() {
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_scan<true>, K4A_THREADS, 0);
+  return nb < 1 ? 1 : nb;
+}
+
+int eval_occupancy() {
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_eval<true, true>, K4B_THREADS, 0);
+  return nb < 1 ? 1 : nb;
+}
+
+void launch_scan(const PhaseArgs &a, const void *tmap, int grid, cudaStream_t s) {
+  static CUtensorMap dummy;
+  if (tmap) k_scan<true><<<grid, K4A_THREADS, 0, s>>>(a, *(const CUtensorMap *)tmap);
+  else k_scan<false><<<grid, K4A_THREADS, 0, s>>>(a, dummy);
+}
+
+void launch_eval(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
+  const bool gated = a.size_mode != 0;
+  if (pixel && gated) k_eval<true, true><<<grid, K4B_THREADS, 0, s>>>(a);
+  else if (pixel) k_eval<true, false><<<grid, K4B_THREADS, 0, s>>>(a);
+  else if (gated) k_eval<false, true><<<grid, K4B_THREADS, 0, s>>>(a);
+  else k_eval<false, false><<<grid, K4B_THREADS, 0, s>>>(a);
+}
+
+void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
+  if (pixel) k_commit<true><<<grid, 256, 0, s>>>(a);
+  else k_commit<false><<<grid, 256, 0, s>>>(a);
+}
+
+}  // namespace rapid

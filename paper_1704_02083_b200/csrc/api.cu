@@ -332,7 +332,9 @@ int build_plan(rapid_ctx *c, int H, int W, const rapid_params *p) {
   if ((rc = ensure(c, c->bsum, N.bsum_total * 8))) return rc;
   if ((rc = ensure(c, c->maps[0], N.map_max * 4))) return rc;
   if ((rc = ensure(c, c->maps[1], N.map_max * 4))) return rc;
-  if ((rc = ensure(c, c->props, N.props_max * 16))) return rc;
+  // proposals: bounded by the phase's blocks, plus the chunked-reservation slack of K4b warps
+  if ((rc = ensure(c, c->props, (N.props_max + (size_t)c->eval_grid * 8 * CAND_SLACK_PER_WARP) * 16)))
+    return rc;
   // candidate list: every block of a phase colour may be a candidate, plus the chunked
   // reservation slack of every scanning warp
   const size_t cand_max = N.props_max + (size_t)c->scan_grid * 8 * CAND_SLACK_PER_WARP;

@@ -285,12 +285,17 @@ __global__ void __launch_bounds__(K4A_THREADS) k_scan(const PhaseArgs a,
 
 // ------------------------------------------------------------------ K4b: evaluate
 template <bool PIXEL, bool GATED>
-__global__ void __launch_bounds__(K4B_THREADS) k_eval(const PhaseArgs a) {
+#ifndef K4B_MIN_BLOCKS
+#define K4B_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(K4B_THREADS, K4B_MIN_BLOCKS) k_eval(const PhaseArgs a) {
   const unsigned long long n = cta_count(a.prev, a.cand_count);
   if (n == 0) return;
   const int lane = lane_id();
   const int nbx = a.st.nbx, nby = a.st.nby;
   unsigned c_prop = 0, c_srej = 0, c_commit = 0;
+  unsigned long long pbase = 0;  // this warp's reserved proposal slots
+  int pleft = 0;
   for (unsigned long long base = blockIdx.x * (unsigned long long)K4B_THREADS; base < n;
        base += (unsigned long long)gridDim.x * K4B_THREADS) {  // warp-uniform trip count
     const unsigned long long i = base + threadIdx.x;
@@ -332,10 +337,10 @@ __global__ void __launch_bounds__(K4B_THREADS) k_eval(const PhaseArgs a) {
           if (u) cb[nb++] = B;
         }
         const Rec recA = a.sp.rec[kb + A];
-        Rec rn[4];
+        int4 rn[4];  // first half of each record (means only): 16 B instead of 32
 #pragma unroll
         for (int k = 0; k < 4; k++)
-          if (k < nb) rn[k] = a.sp.rec[kb + cb[k]];
+          if (k < nb) rn[k] = __ldg(reinterpret_cast<const int4 *>(&a.sp.rec[kb + cb[k]]));
         const RecV ra = rec_vals(recA);
         bool have = false;
         i128 bestE = 0;
@@ -348,7 +353,13 @@ __global__ void __launch_bounds__(K4B_THREADS) k_eval(const PhaseArgs a) {
 #pragma unroll
           for (int r = 0; r < 4; r++)
             if (nq[r] >= 0) dB2 += ew[r] * ((long long)(nq[r] != B) - (long long)(nq[r] != A));
-          const i128 E = delta_e(ra, rec_vals(rn[k]), d, 2 * dB2, a.lam_pos, a.lam_b);
+          RecV rb;
+          rb.c0 = (unsigned)rn[k].z & 0xffffu;
+          rb.c1 = (unsigned)rn[k].z >> 16;
+          rb.c2 = (unsigned)rn[k].w & 0xffffu;
+          rb.mx = rn[k].x;
+          rb.my = rn[k].y;
+          const i128 E = delta_e(ra, rb, d, 2 * dB2, a.lam_pos, a.lam_b);
           if (!have || E < bestE || (E == bestE && B < bestB)) {
             have = true;
             bestE = E;
@@ -381,14 +392,23 @@ __global__ void __launch_bounds__(K4B_THREADS) k_eval(const PhaseArgs a) {
         c_commit += __popc(pm);
       } else {
         agg_add_i32(prop, kb + A, (int)d[0], a.sp.out);
-        unsigned long long pb = 0;
-        if (lane == 0) pb = atomicAdd(a.prop_count, (unsigned long long)__popc(pm));
-        pb = __shfl_sync(FULL, pb, 0);
+        const int np = __popc(pm);
+        if (np > pleft) {  // retire the rest of the chunk (sentinels), reserve a new one
+          if (lane < pleft) a.props[pbase + lane] = make_uint4(0u, 0xffffffffu, 0u, 0u);
+          unsigned long long nb = 0;
+          if (lane == 0) nb = atomicAdd(a.prop_count, (unsigned long long)CHUNK);
+          pbase = __shfl_sync(FULL, nb, 0);
+          pleft = CHUNK;
+        }
         if (prop)
-          a.props[pb + __popc(pm & lanemask_lt())] = make_uint4((unsigned)idx, (unsigned)A, (unsigned)Bm, rgb);
+          a.props[pbase + __popc(pm & lanemask_lt())] = make_uint4((unsigned)idx, (unsigned)A, (unsigned)Bm, rgb);
+        pbase += np;
+        pleft -= np;
       }
     }
   }
+  if (lane < pleft) a.props[pbase + lane] = make_uint4(0u, 0xffffffffu, 0u, 0u);
+  if (lane + 32 < pleft) a.props[pbase + lane + 32] = make_uint4(0u, 0xffffffffu, 0u, 0u);
   if (lane == 0) {
     if (c_prop) atomicAdd(&a.cnt[2], (unsigned long long)c_prop);
     if (c_srej) atomicAdd(&a.cnt[3], (unsigned long long)c_srej);
@@ -409,8 +429,8 @@ __global__ void __launch_bounds__(256) k_commit(const PhaseArgs a) {
     bool ok = false, rej = false;
     int A = 0, B = 0, kb = 0;
     long long d[6] = {0, 0, 0, 0, 0, 0};
-    if (valid) {
-      const uint4 pr = a.props[i];
+    const uint4 pr = valid ? a.props[i] : make_uint4(0u, 0xffffffffu, 0u, 0u);
+    if (pr.y != 0xffffffffu) {  // skip unused reserved slots
       const size_t idx = pr.x;
       A = (int)pr.y;
       B = (int)pr.z;

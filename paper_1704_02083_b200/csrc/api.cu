@@ -357,6 +357,9 @@ StageDev stage_dev(rapid_ctx *c, int s, int32_t *labels_out) {
   d.b = S.b;
   d.tiles_x = S.tiles_x;
   d.tiles_y = S.tiles_y;
+  d.uniform = 1;
+  for (size_t i = 0; i < S.xs.size() && d.uniform; i++) d.uniform = S.xs[i] == (int32_t)(i * S.b);
+  for (size_t j = 0; j < S.ys.size() && d.uniform; j++) d.uniform = S.ys[j] == (int32_t)(j * S.b);
   d.fd_tx = make_fastdiv((uint32_t)S.tiles_x);
   d.fd_ty = make_fastdiv((uint32_t)S.tiles_y);
   d.xs = T + S.o_xs;

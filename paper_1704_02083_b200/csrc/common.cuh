@@ -52,6 +52,7 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
 
 struct StageDev {
   int32_t nbx, nby, b;
+  int32_t uniform;               // 1: every block is b x b with xs[i] = i*b, ys[j] = j*b
   int32_t tiles_x, tiles_y;      // sweep tiles per image
   FastDiv fd_tx, fd_ty;          // division by tiles_x / tiles_y
   const int32_t *xs, *ys;        // block boundaries (nbx+1, nby+1)

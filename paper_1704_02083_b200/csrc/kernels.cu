@@ -59,6 +59,43 @@ __global__ void k_pyramid_leaf(const StageDev st, const uint8_t *__restrict__ im
   }
 }
 
+// K1 fast path: uniform 2x2 leaf, W % 8 == 0.  A thread sums 4 consecutive blocks of one
+// block row from two 24-B pixel segments (8-B vector loads) and writes 4 packed sums.
+__device__ __forceinline__ uint32_t byte_of(const uint2 (&v)[3], int i) {
+  const uint32_t w = (i < 8) ? ((i < 4) ? v[0].x : v[0].y) : (i < 16) ? ((i < 12) ? v[1].x : v[1].y)
+                                                                      : ((i < 20) ? v[2].x : v[2].y);
+  return (w >> (8 * (i & 3))) & 0xffu;
+}
+__global__ void k_pyramid_leaf2(const StageDev st, const uint8_t *__restrict__ image, int H, int W,
+                                int B, uint64_t *__restrict__ bsum) {
+  const int q = st.nbx / 4;  // thread groups per block row
+  const size_t n = (size_t)q * st.nby * B;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = t / q;  // img * nby + gy
+    const int gx = (int)(t - row * q) * 4;
+    const int img = (int)(row / st.nby), gy = (int)(row - (size_t)img * st.nby);
+    const uint8_t *p0 = image + (((size_t)img * H + 2 * gy) * W + 2 * gx) * 3;
+    const uint2 *r0 = reinterpret_cast<const uint2 *>(p0);
+    const uint2 *r1 = reinterpret_cast<const uint2 *>(p0 + (size_t)W * 3);
+    const uint2 a[3] = {__ldg(r0), __ldg(r0 + 1), __ldg(r0 + 2)};
+    const uint2 b[3] = {__ldg(r1), __ldg(r1 + 1), __ldg(r1 + 2)};
+    uint64_t out[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      uint32_t s[3];
+#pragma unroll
+      for (int ch = 0; ch < 3; ch++)
+        s[ch] = byte_of(a, 6 * j + ch) + byte_of(a, 6 * j + 3 + ch) + byte_of(b, 6 * j + ch) +
+                byte_of(b, 6 * j + 3 + ch);
+      out[j] = (uint64_t)s[0] | ((uint64_t)s[1] << 21) | ((uint64_t)s[2] << 42);
+    }
+    uint64_t *dst = bsum + row * st.nbx + gx;
+    reinterpret_cast<ulonglong2 *>(dst)[0] = make_ulonglong2(out[0], out[1]);
+    reinterpret_cast<ulonglong2 *>(dst)[1] = make_ulonglong2(out[2], out[3]);
+  }
+}
+
 // K1: coarser stage from its <= 2x2 children (packed fields never overflow: block <= 64^2).
 __global__ void k_pyramid_up(const StageDev st, const StageDev ch, int B, uint64_t *__restrict__ bsum) {
   const size_t nper = (size_t)st.nbx * st.nby;
@@ -250,6 +287,16 @@ __device__ void hash_add(const MergeArgs &a, int V, int T, unsigned e) {
   const unsigned long long key = ((unsigned long long)(unsigned)V << 32) | (unsigned)T;
   unsigned long long h = hmix(key) & a.hmask;
   while (true) {
+    // most calls find an existing key: a plain (volatile) read avoids contended CAS
+    const unsigned long long seen = *reinterpret_cast<volatile unsigned long long *>(&a.hkeys[h]);
+    if (seen == key) {
+      atomicAdd(&a.hvals[h], e);
+      return;
+    }
+    if (seen != HEMPTY) {
+      h = (h + 1) & a.hmask;
+      continue;
+    }
     const unsigned long long old = atomicCAS(&a.hkeys[h], HEMPTY, key);
     if (old == HEMPTY) {
       atomicAdd(&a.hvals[h], e);
@@ -582,19 +629,34 @@ __global__ void __launch_bounds__(256) k_transition(const TransArgs a) {
   const bool rm = *a.remap_pending != 0u;
   const int32_t *pmap = pv.map + (size_t)img * pv.nby * pv.nbx;
   int32_t *nmap = nx.map + (size_t)img * nx.nby * nx.nbx;
+  // each thread: 4 consecutive children of one row (16 threads per 64-wide tile row)
   int act = 0;
-  int last = -1;
-  for (int k = threadIdx.x; k < TX * TY; k += 256) {
-    const int gx = tx * TX + (k % TX), gy = ty * TY + (k / TX);
-    int l = -1;
-    if (gx < nx.nbx && gy < nx.nby) {
-      l = pmap[(size_t)nx.py[gy] * pv.nbx + nx.px[gx]];
-      if (rm && !a.sp.alive[kb + l]) l = a.sp.remap[kb + l];
-      nmap[(size_t)gy * nx.nbx + gx] = l;
-      if (a.gate && l != last) {
-        act |= a.sp.active[kb + l];
-        last = l;
+  const int gx = tx * TX + 4 * (threadIdx.x & 15), gy = ty * TY + (threadIdx.x >> 4);
+  if (gy < nx.nby && gx < nx.nbx) {
+    const int32_t *prow = pmap + (size_t)nx.py[gy] * pv.nbx;
+    const int4 pc = *reinterpret_cast<const int4 *>(nx.px + gx);  // tables are 16-B padded
+    int l[4] = {prow[pc.x], -1, -1, -1};
+#pragma unroll
+    for (int u = 1; u < 4; u++)
+      if (gx + u < nx.nbx) l[u] = prow[(&pc.x)[u]];
+    int last = -1, res = -1;
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      if (l[u] < 0) continue;
+      if (l[u] != last) {  // remap / activity once per distinct parent label
+        last = l[u];
+        res = (rm && !a.sp.alive[kb + last]) ? a.sp.remap[kb + last] : last;
+        if (a.gate) act |= a.sp.active[kb + res];
       }
+      l[u] = res;
+    }
+    int32_t *dst = nmap + (size_t)gy * nx.nbx + gx;
+    if (gx + 3 < nx.nbx && (nx.nbx & 3) == 0) {
+      *reinterpret_cast<int4 *>(dst) = make_int4(l[0], l[1], l[2], l[3]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (gx + u < nx.nbx) dst[u] = l[u];
     }
   }
   if (a.gate) {
@@ -724,7 +786,10 @@ void launch_init_sp(const InitArgs &a, cudaStream_t s) {
 void launch_pyramid_leaf(const StageDev &st, const uint8_t *image, int H, int W, int B,
                          uint64_t *bsum, cudaStream_t s) {
   const size_t n = (size_t)st.nbx * st.nby * B;
-  k_pyramid_leaf<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(st, image, H, W, B, bsum);
+  if (st.uniform && st.b == 2 && W % 8 == 0 && ((uintptr_t)image & 7u) == 0)
+    k_pyramid_leaf2<<<grid_for(n / 4, 256, 148 * 32), 256, 0, s>>>(st, image, H, W, B, bsum);
+  else
+    k_pyramid_leaf<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(st, image, H, W, B, bsum);
 }
 
 void launch_pyramid_up(const StageDev &parent, const StageDev &child, int B, uint64_t *bsum,

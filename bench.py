@@ -285,25 +285,38 @@ def run_ours(args):
     if rank == 0:
         peak, peak_src = peaks()
         pb = phase_bytes(info, w, window)
-        # dominant kernel: the propose sweep (K4); algorithmic bytes per launch / average launch time
-        kbytes = sum(v[0] for v in pb.values())
-        kms = float(prof_ms[rb.K_PROPOSE].sum())
-        klaunch = int(prof_launch[rb.K_PROPOSE].sum())
-        share = kms / max(1e-9, float(prof_ms[[rb.K_PYRAMID, rb.K_SNAPSHOT, rb.K_PROPOSE, rb.K_COMMIT, rb.K_MERGE,
-                                                 rb.K_PREDICT, rb.K_TRANSITION, rb.K_FINAL]].sum()))
-        achieved = kbytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
-        px_stage = len(p.block_sizes) - 1
+        # Dominant HBM kernel: the K4a scan at the pixel stage (the last stage).  Its algorithmic
+        # bytes per launch are the label reads of the phase's window: 4 B x window blocks
+        # (SURVEY §8(d)); colour reads and label writes belong to K4b/K5 and enter the phase-set
+        # figure below.
+        ps = len(p.block_sizes) - 1
+        runs = int(info.stage_sweeps_run[ps]) * 4
+        scan_bytes = 4 * window[ps] * runs
+        scan_ms = float(prof_ms[rb.K_PROPOSE][ps])
+        scan_launch = int(prof_launch[rb.K_PROPOSE][ps])
+        steps_ms = float(prof_ms[[rb.K_PYRAMID, rb.K_SNAPSHOT, rb.K_PROPOSE, rb.K_COMMIT, rb.K_MERGE, rb.K_PREDICT,
+                                  rb.K_TRANSITION, rb.K_FINAL, rb.K_EVAL]].sum())
+        achieved = scan_bytes / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else 0.0
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", "scan_traffic.json")
+        if os.path.exists(tfile):  # ncu dram bytes of one pixel-stage k_scan launch (committed capture)
+            with open(tfile) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        all_bytes = sum(v[0] for v in pb.values())
+        phase_ms = float(prof_ms[rb.K_PHASESET].sum())
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": None,
-                "kernel": "k_propose (K4 parity-phase sweep), all stages",
-                "bytes_per_launch": round(kbytes / max(1, klaunch)),
-                "avg_launch_ms": round(kms / max(1, klaunch), 4), "launches": klaunch,
-                "share_of_step": round(share, 4), "peak_source": peak_src,
-                "pixel_stage": {"achieved": round(pb[px_stage][0] / (prof_ms[rb.K_PROPOSE][px_stage] / 1e3) / 1e9, 1)
-                                if prof_ms[rb.K_PROPOSE][px_stage] > 0 else None,
-                                "avg_launch_ms": round(float(prof_ms[rb.K_PROPOSE][px_stage]) / max(1, prof_launch[rb.K_PROPOSE][px_stage]), 4)},
-                "phase_set_GBps": round(kbytes / (float(prof_ms[rb.K_PHASESET].sum()) / 1e3) / 1e9, 1)
-                if prof_ms[rb.K_PHASESET].sum() > 0 else None}
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "kernel": f"k_scan (K4a, TMA-streamed parity-phase scan), pixel stage ({scan_launch} launches/step)",
+                "bytes_per_launch": round(scan_bytes / max(1, scan_launch)),
+                "avg_launch_ms": round(scan_ms / max(1, scan_launch), 4),
+                "share_of_step": round(scan_ms / max(1e-9, steps_ms), 4), "peak_source": peak_src,
+                "bytes_model": "4 B x blocks within Chebyshev distance 1 of a block with an active label, per phase",
+                "all_stages_scan_GBps": round(sum(4 * window[s] * int(info.stage_sweeps_run[s]) * 4
+                                                  for s in range(ps + 1)) /
+                                              (float(prof_ms[rb.K_PROPOSE].sum()) / 1e3) / 1e9, 1),
+                "phase_set": {"GBps": round(all_bytes / (phase_ms / 1e3) / 1e9, 1) if phase_ms > 0 else None,
+                              "kernels": "snapshot + K4a scan + K4b eval + K5 commit, all stages",
+                              "bytes_model": "4 B x window + c_s x topology-passing candidates + 4 B x commits"}}
         line = {"metric": METRIC, "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
@@ -312,9 +325,10 @@ def run_ours(args):
                 "roofline": roof, "e2e": e2e, "gpu_launches": total_launches * args.steps,
                 "clocks": ck,
                 "per_kernel_ms_per_step": {nm: round(float(prof_ms[k].sum()), 3) for k, nm in enumerate(
-                    ["pyramid", "snapshot", "propose", "commit", "merge", "predict", "transition", "final",
-                     "phase_set"])},
-                "stage_propose_ms": [round(float(x), 3) for x in prof_ms[rb.K_PROPOSE][:len(p.block_sizes)]],
+                    ["pyramid", "snapshot", "scan", "commit", "merge", "predict", "transition", "final",
+                     "phase_set", "eval"])},
+                "stage_scan_ms": [round(float(x), 3) for x in prof_ms[rb.K_PROPOSE][:len(p.block_sizes)]],
+                "stage_eval_ms": [round(float(x), 3) for x in prof_ms[rb.K_EVAL][:len(p.block_sizes)]],
                 "stage_sweeps_run": [int(x) for x in info.stage_sweeps_run[:len(p.block_sizes)]],
                 "alive": int(info.alive), "active": int(info.active)}
         if not args.no_cpu:

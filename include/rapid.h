@@ -134,8 +134,9 @@ typedef struct {
 #define RAPID_K_PREDICT 5
 #define RAPID_K_TRANSITION 6
 #define RAPID_K_FINAL 7
-#define RAPID_K_PHASESET 8 /* snapshot+propose+commit of every phase of the stage, as one interval */
-#define RAPID_NK 9
+#define RAPID_K_PHASESET 8 /* snapshot+scan+eval+commit of every phase of the stage, as one interval */
+#define RAPID_K_EVAL 9     /* K4b candidate evaluation (RAPID_K_PROPOSE is the K4a scan) */
+#define RAPID_NK 10
 typedef struct {
   uint64_t launches[RAPID_NK][RAPID_MAX_STAGES];
   double ms[RAPID_NK][RAPID_MAX_STAGES];

@@ -105,6 +105,10 @@ def lib():
         L.orc_yokoi_c4.restype = ctypes.c_int
         L.orc_round_mean.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
         L.orc_round_mean.restype = None
+        L.orc_block_move.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.POINTER(OrcParams), ctypes.POINTER(ctypes.c_int32),
+                                     ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_uint64)]
+        L.orc_block_move.restype = ctypes.c_int
         _LIB = L
     return _LIB
 
@@ -218,6 +222,21 @@ def stage_axis(length, b, cuts):
 
 def yokoi_c4(mask):
     return lib().orc_yokoi_c4(mask)
+
+
+def block_move(win, means, d, e, params):
+    """One block's decision (O6 steps 2-6, no gates). win: 9 labels row-major (-1 outside);
+    means: [9][5] (cq r,g,b, mq x,y) of each cell's label; d: [6] block data; e: [4] edges
+    N,E,S,W.  Returns (code, B, dE): code 0 not boundary, 1 not simple, 2 no move, 3 move."""
+    w = np.ascontiguousarray(win, dtype=np.int32)
+    m = np.ascontiguousarray(means, dtype=np.int64)
+    dd = np.ascontiguousarray(d, dtype=np.int64)
+    ee = np.ascontiguousarray(e, dtype=np.int64)
+    B, hi, lo = ctypes.c_int32(-1), ctypes.c_int64(0), ctypes.c_uint64(0)
+    op = make_params(params)
+    code = lib().orc_block_move(w.ctypes.data, m.ctypes.data, dd.ctypes.data, ee.ctypes.data,
+                                ctypes.byref(op), ctypes.byref(B), ctypes.byref(hi), ctypes.byref(lo))
+    return code, B.value, i128(hi.value, lo.value) if code == 3 else None
 
 
 def round_mean(S, n):

@@ -198,6 +198,93 @@ static void delta_cp(const seg_t *g, int A, int B, const int64_t d[6], i128 *dC,
   *dP = q;
 }
 
+/* O6 steps 4-6 for one block with label A, 4-neighbour labels nq (N,E,S,W; -1 = none),
+ * shared edge lengths eq and block data d: candidates are the distinct neighbour labels
+ * other than A (A8); dE (Eq. 1 with Eq. 2, frozen quantised means from `means`) per
+ * candidate; argmin with ties to the smallest label (A7).  Returns 0 if no candidate. */
+typedef void (*means_fn)(const void *ctx, int32_t label, int64_t m[5]);
+
+static int argmin_move(const orc_params *p, int32_t A, const int32_t nq[4], const int64_t eq[4],
+                       const int64_t d[6], means_fn means, const void *ctx, int32_t *B_out, i128 *E_out) {
+  int64_t mA[5];
+  means(ctx, A, mA);
+  int have = 0;
+  int32_t bestB = -1;
+  i128 bestE = 0;
+  for (int q = 0; q < 4; q++) {
+    int32_t B = nq[q];
+    if (B < 0 || B == A) continue;
+    int dup = 0;
+    for (int r = 0; r < q; r++)
+      if (nq[r] == B) dup = 1;
+    if (dup) continue;
+    int64_t mB[5];
+    means(ctx, B, mB);
+    i128 dC = 0, dP = 0, dB2 = 0;
+    for (int ch = 0; ch < 3; ch++) /* E_col: n(cB^2 - cA^2) - 2^(F+1) S (cB - cA) */
+      dC += (i128)d[0] * ((i128)mB[ch] * mB[ch] - (i128)mA[ch] * mA[ch]) -
+            ((i128)d[1 + ch] << (FRAC + 1)) * ((i128)mB[ch] - mA[ch]);
+    for (int k = 0; k < 2; k++) /* E_pos, same form with the position means */
+      dP += (i128)d[0] * ((i128)mB[3 + k] * mB[3 + k] - (i128)mA[3 + k] * mA[3 + k]) -
+            ((i128)d[4 + k] << (FRAC + 1)) * ((i128)mB[3 + k] - mA[3 + k]);
+    for (int r = 0; r < 4; r++)
+      if (nq[r] >= 0) dB2 += (i128)eq[r] * ((nq[r] != B) - (nq[r] != A));
+    dB2 *= 2; /* ordered pairs (A3) */
+    i128 E = weigh(p, dC, dP, dB2);
+    if (!have || E < bestE || (E == bestE && B < bestB)) {
+      have = 1; bestE = E; bestB = B;
+    }
+  }
+  *B_out = bestB;
+  *E_out = bestE;
+  return have;
+}
+
+static void seg_means(const void *ctx, int32_t l, int64_t m[5]) {
+  const seg_t *g = (const seg_t *)ctx;
+  for (int ch = 0; ch < 3; ch++) m[ch] = g->cq[(size_t)l * 3 + ch];
+  for (int k = 0; k < 2; k++) m[3 + k] = g->mq[(size_t)l * 2 + k];
+}
+
+typedef struct { const int32_t *labels; const int64_t *means; } win_means_t;
+static void win_means(const void *ctx, int32_t l, int64_t m[5]) {
+  const win_means_t *w = (const win_means_t *)ctx;
+  for (int c = 0; c < 9; c++)
+    if (w->labels[c] == l) {
+      memcpy(m, w->means + 5 * c, 5 * sizeof(int64_t));
+      return;
+    }
+  memset(m, 0, 5 * sizeof(int64_t));
+}
+
+/* One block's O6 decision in isolation (sampled parity checks at sizes the whole oracle cannot
+ * run): win = 3x3 labels row-major (-1 = outside), means of each window cell's label
+ * (cq_r, cq_g, cq_b, mq_x, mq_y in 2^F units), block data d, edge lengths e (N, E, S, W).
+ * Returns 0 not a boundary block, 1 not a simple point, 2 no move (min dE >= 0), 3 move to
+ * *B_out with *dE (hi/lo of the int128).  No mask gate, no size gate. */
+int orc_block_move(const int32_t *win, const int64_t *means, const int64_t *d, const int64_t *e,
+                   const orc_params *p, int32_t *B_out, int64_t *dE_hi, uint64_t *dE_lo) {
+  const int32_t A = win[4];
+  const int32_t nq[4] = {win[1], win[5], win[7], win[3]}; /* N, E, S, W */
+  int bnd = 0;
+  for (int q = 0; q < 4; q++)
+    if (nq[q] >= 0 && nq[q] != A) bnd = 1;
+  if (!bnd) return 0;
+  static const int RING[8] = {1, 2, 5, 8, 7, 6, 3, 0}; /* N NE E SE S SW W NW in the 3x3 */
+  int mask = 0;
+  for (int k = 0; k < 8; k++)
+    if (win[RING[k]] >= 0 && win[RING[k]] == A) mask |= 1 << k;
+  if (orc_yokoi_c4(mask) != 1) return 1;
+  win_means_t wm = {win, means};
+  int32_t B;
+  i128 E;
+  if (!argmin_move(p, A, nq, e, d, win_means, &wm, &B, &E) || !(E < 0)) return 2;
+  *B_out = B;
+  *dE_hi = (int64_t)(E >> 64);
+  *dE_lo = (uint64_t)E;
+  return 3;
+}
+
 static void dump_state(seg_t *g) {
   orc_debug *dbg = g->dbg;
   const stage_t *st = &g->st[g->cur];
@@ -262,27 +349,9 @@ static int run_phase(seg_t *g, int s, int t, int ph, prop_t *props) {
       /* 4./5./6. candidates = distinct 4-neighbour labels (A8); Eq. 3 argmin (A7) */
       int64_t d[6];
       block_data(g, s, i, j, d);
-      int have = 0;
       int32_t bestB = -1;
       i128 bestE = 0;
-      for (int q = 0; q < 4; q++) {
-        int32_t B = nq[q];
-        if (B < 0 || B == A) continue;
-        int dup = 0;
-        for (int r = 0; r < q; r++)
-          if (nq[r] == B) dup = 1;
-        if (dup) continue;
-        i128 dC, dP, dB2 = 0;
-        delta_cp(g, A, B, d, &dC, &dP);
-        for (int r = 0; r < 4; r++)
-          if (nq[r] >= 0) dB2 += (i128)eq[r] * ((nq[r] != B) - (nq[r] != A));
-        dB2 *= 2; /* ordered pairs (A3) */
-        i128 E = weigh(p, dC, dP, dB2);
-        if (!have || E < bestE || (E == bestE && B < bestB)) {
-          have = 1; bestE = E; bestB = B;
-        }
-      }
-      if (!have || !(bestE < 0)) continue;
+      if (!argmin_move(p, A, nq, eq, d, seg_means, g, &bestB, &bestE) || !(bestE < 0)) continue;
       /* 7. size gate for the desired move (A12) */
       if (p->size_mode != ORC_SIZE_NONE) {
         if ((i128)(g->nsnap[A] - d[0]) * p->l_den < (i128)p->l_num * g->init[A]) {

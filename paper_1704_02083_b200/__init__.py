@@ -19,9 +19,10 @@ MAX_STAGES = 12
 MAX_SWEEPS = 64
 MAX_PROTO = 4
 NCNT = 6
-NK = 9
+NK = 10
 C_CAND, C_TOPO, C_PROP, C_SIZEREJ, C_COMMIT, C_COMMREJ = range(6)
-K_PYRAMID, K_SNAPSHOT, K_PROPOSE, K_COMMIT, K_MERGE, K_PREDICT, K_TRANSITION, K_FINAL, K_PHASESET = range(9)
+(K_PYRAMID, K_SNAPSHOT, K_PROPOSE, K_COMMIT, K_MERGE, K_PREDICT, K_TRANSITION, K_FINAL, K_PHASESET,
+ K_EVAL) = range(10)  # K_PROPOSE = K4a scan (the HBM-streaming kernel), K_EVAL = K4b
 STOP_NONE, STOP_PHASE, STOP_STAGE_START, STOP_AFTER_MERGE, STOP_AFTER_PREDICT = range(5)
 STATUS = {0: "ok", -1: "E_ARG", -2: "E_CAPACITY", -3: "E_RANGE", -4: "E_CUDA", -5: "E_OOM",
           -6: "E_INTEGRITY", -7: "E_STATE"}

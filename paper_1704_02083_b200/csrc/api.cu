@@ -568,8 +568,11 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           {
             Timer t2(c, s, RAPID_K_PROPOSE, st);
             launch_scan(pa, has_tmap[st] ? tmaps[st].b : nullptr, c->scan_grid, s);
-            launch_eval(pa, pixel, c->eval_grid, s);
             c->launches++;
+          }
+          {
+            Timer t2(c, s, RAPID_K_EVAL, st);
+            launch_eval(pa, pixel, c->eval_grid, s);
             c->launches++;
           }
           if (gated_sz) {

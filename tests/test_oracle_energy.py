@@ -331,3 +331,42 @@ def test_mask_rules_restrict_candidates():
         r = oracle.segment(img, q)
         cands[rule] = r.counters[1, 0, 0, oracle.C_CAND]
     assert cands[3] <= cands[2] <= cands[0]
+
+
+def test_block_move_matches_full_phase():
+    """orc_block_move (used for sampled checks at full scale) reproduces a whole phase of the
+    oracle: from the state before phase (s,t,ph), every block of the phase colour moves exactly
+    as in the full run (NONE, mask OFF)."""
+    w = synth.config(1)
+    img = w.images()[0]
+    p = copy.deepcopy(w.params)
+    geo = brute.geometry(w.H, w.W, p.n_superpixels, p.block_sizes)
+    checked = moved = 0
+    for (s, t, ph) in [(4, 0, 1), (4, 1, 2), (3, 0, 3)]:
+        bmap, sums, _ = state(img, p, before_key(p, s, t, ph))
+        amap, _, _ = state(img, p, (oracle.STOP_PHASE, s, t, ph))
+        xs, ys = geo[s]
+        cq, mq = brute.quantised_means(sums)
+        H, W = bmap.shape
+        for j in range(ph >> 1, H, 2):
+            for i in range(ph & 1, W, 2):
+                win = np.full(9, -1, dtype=np.int32)
+                for dy in (-1, 0, 1):
+                    for dx in (-1, 0, 1):
+                        if 0 <= i + dx < W and 0 <= j + dy < H:
+                            win[(dy + 1) * 3 + dx + 1] = bmap[j + dy, i + dx]
+                means = np.zeros((9, 5), dtype=np.int64)
+                for c in range(9):
+                    if win[c] >= 0:
+                        means[c] = [*cq[win[c]], *mq[win[c]]]
+                x0, x1, y0, y1 = xs[i], xs[i + 1], ys[j], ys[j + 1]
+                blk = img[y0:y1, x0:x1].reshape(-1, 3).astype(np.int64)
+                yy, xx = np.mgrid[y0:y1, x0:x1]
+                d = [blk.shape[0], *blk.sum(0), int(xx.sum()), int(yy.sum())]
+                e = [x1 - x0, y1 - y0, x1 - x0, y1 - y0]
+                code, B, dE = oracle.block_move(win, means, d, e, p)
+                want = B if code == 3 else bmap[j, i]
+                assert amap[j, i] == want, (s, t, ph, i, j)
+                checked += 1
+                moved += code == 3
+    assert moved > 50 and checked > 5000

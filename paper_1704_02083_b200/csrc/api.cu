@@ -91,11 +91,12 @@ struct rapid_ctx {
   uint32_t *mlock = nullptr, *res = nullptr;
   Ctl *ctl = nullptr;
   // plan-sized buffers
-  DevBuf tab, bsum, maps[2], props, work, cands;
+  DevBuf tab, bsum, maps[2], props, work, cands, bset;
   // host-API staging
   DevBuf himg, hlab;
   // occupancy
-  int scan_grid = 0, eval_grid = 0;  // persistent grid sizes (CTAs)
+  int scan_grid = 0, eval_grid = 0, sweep_grid = 0;  // persistent grid sizes (CTAs)
+  bool use_bset = true;  // RAPID_SWEEP=scan selects the full-scan path K4a + K4b (A/B testing)
   bool use_tma = true;  // RAPID_NO_TMA=1 forces the LDG tile loader (A/B testing)
   // profiling
   int prof = 0;  // 0 off, 1 events, 2 events + window counting
@@ -333,13 +334,14 @@ int build_plan(rapid_ctx *c, int H, int W, const rapid_params *p) {
   if ((rc = ensure(c, c->maps[0], N.map_max * 4))) return rc;
   if ((rc = ensure(c, c->maps[1], N.map_max * 4))) return rc;
   // proposals: bounded by the phase's blocks, plus the chunked-reservation slack of K4b warps
-  if ((rc = ensure(c, c->props, (N.props_max + (size_t)c->eval_grid * 8 * CAND_SLACK_PER_WARP) * 16)))
+  if ((rc = ensure(c, c->props, (N.props_max + (size_t)std::max(c->eval_grid, c->sweep_grid) * 8 * CAND_SLACK_PER_WARP) * 16)))
     return rc;
   // candidate list: every block of a phase colour may be a candidate, plus the chunked
   // reservation slack of every scanning warp
   const size_t cand_max = N.props_max + (size_t)c->scan_grid * 8 * CAND_SLACK_PER_WARP;
   if ((rc = ensure(c, c->cands, cand_max * 32))) return rc;
   if ((rc = ensure(c, c->work, N.tiles_max * 4))) return rc;
+  if ((rc = ensure(c, c->bset, N.tiles_max * 32 * 4))) return rc;  // 1 bit per block
   cudaError_t e = cudaMemcpy(c->tab.p, N.tab.data(), N.tab.size() * 4, cudaMemcpyHostToDevice);
   if ((rc = cuda_check(c, e, "upload tables"))) return rc;
   N.valid = true;
@@ -521,6 +523,20 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
         launch_recount(ra, pixel, grid_k, s, &c->launches);
       }
     }
+    const int gating = (st > 0 && mask != RAPID_MASK_OFF) ? (mask == RAPID_MASK_EQ7 ? 2 : 1) : 0;
+    if (c->use_bset) {  // boundary sets of the stage (maintained by the commits from here on)
+      Timer tm(c, s, RAPID_K_TRANSITION, st);
+      PhaseArgs ba{};
+      ba.st = sd[st];
+      ba.sp = sp;
+      ba.B = B; ba.M = M;
+      ba.gating = gating;
+      ba.worklist = use_work ? (const int32_t *)c->work.p : nullptr;
+      ba.nwork = &ctl->nwork[st];
+      ba.bset = (uint32_t *)c->bset.p;
+      launch_bset_build(ba, c->sm_count * 8, s);
+      c->launches++;
+    }
     if (c->prof >= 2 && use_work) {  // profiling only: algorithmic window of the gated stage
       launch_count_window(sd[st], sp, B, M, &ctl->stage_info[st][2], s);
       c->launches++;
@@ -549,7 +565,15 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           pa.H = H; pa.W = W; pa.B = B; pa.M = M;
           pa.cx = ph & 1;
           pa.cy = ph >> 1;
-          pa.gating = (st > 0 && mask != RAPID_MASK_OFF) ? (mask == RAPID_MASK_EQ7 ? 2 : 1) : 0;
+          pa.gating = gating;
+          pa.bset = c->use_bset ? (uint32_t *)c->bset.p : nullptr;
+          {  // enough warp iterations to occupy every sweep warp twice (tile count upper bound)
+            const size_t words = (size_t)sd[st].tiles_x * sd[st].tiles_y * B * (TY / 2);
+            const size_t warps = (size_t)c->sweep_grid * 8;
+            int G = 32;
+            while (G > 4 && words / G < 2 * warps) G >>= 1;
+            pa.gwords = G;
+          }
           pa.size_mode = (int)p->size_mode;
           pa.l_num = p->l_num; pa.l_den = p->l_den;
           pa.lam_pos = p->lambda_pos_q16;
@@ -565,15 +589,21 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           pa.prev = t > 0 ? &ctl->cnt[st][t - 1][0][0] : nullptr;
           pa.victim_any = &ctl->victim_any[st];
           if (gated_sz) cudaMemsetAsync(c->out, 0, sizeof(int32_t) * K, s);
-          {
+          if (c->use_bset) {
             Timer t2(c, s, RAPID_K_PROPOSE, st);
-            launch_scan(pa, has_tmap[st] ? tmaps[st].b : nullptr, c->scan_grid, s);
+            launch_sweep(pa, pixel, c->sweep_grid, s);
             c->launches++;
-          }
-          {
-            Timer t2(c, s, RAPID_K_EVAL, st);
-            launch_eval(pa, pixel, c->eval_grid, s);
-            c->launches++;
+          } else {
+            {
+              Timer t2(c, s, RAPID_K_PROPOSE, st);
+              launch_scan(pa, has_tmap[st] ? tmaps[st].b : nullptr, c->scan_grid, s);
+              c->launches++;
+            }
+            {
+              Timer t2(c, s, RAPID_K_EVAL, st);
+              launch_eval(pa, pixel, c->eval_grid, s);
+              c->launches++;
+            }
           }
           if (gated_sz) {
             Timer t2(c, s, RAPID_K_COMMIT, st);
@@ -704,7 +734,7 @@ void rapid_free(rapid_ctx *c) {
                   c->vlist, c->alist, c->pairs, c->alive, c->active, c->victim, c->y, c->dirty,
                   c->deg, c->chunk, c->hkeys, c->candE, c->hvals, c->hnext, c->candT, c->ctl,
                   c->candV, c->mlock, c->res,
-                  c->tab.p, c->bsum.p, c->maps[0].p, c->maps[1].p, c->props.p, c->work.p, c->cands.p,
+                  c->tab.p, c->bsum.p, c->maps[0].p, c->maps[1].p, c->props.p, c->work.p, c->cands.p, c->bset.p,
                   c->himg.p, c->hlab.p};
   for (void *q : ptrs)
     if (q) cudaFree(q);
@@ -755,6 +785,11 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   cudaMemset(c->rc, 0, K * SUMW * 8);
   c->scan_grid = c->sm_count * scan_occupancy();
   c->eval_grid = c->sm_count * eval_occupancy();
+  c->sweep_grid = c->sm_count * sweep_occupancy();
+  {
+    const char *e = getenv("RAPID_SWEEP");
+    c->use_bset = !(e && strcmp(e, "scan") == 0);
+  }
   {
     const char *e = getenv("RAPID_NO_TMA");
     c->use_tma = !(e && e[0] == '1');

@@ -25,6 +25,8 @@ struct PhaseArgs {
   unsigned long long *cnt;        // [NCNT] counters of this phase
   const unsigned long long *prev; // counters of the previous sweep (phase 0), or null
   uint32_t *victim_any;
+  uint32_t *bset;            // boundary sets of the stage (null: full-scan path K4a/K4b)
+  int32_t gwords;            // k_sweep: bset words per warp iteration (4..32)
 };
 
 struct SnapArgs {
@@ -132,6 +134,10 @@ void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s);
 void launch_scan(const PhaseArgs &a, const void *tmap, int grid, cudaStream_t s);
 void launch_eval(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
 void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
+// boundary-set sweep: K4 build (once per stage) and the fused bitset-driven sweep
+void launch_bset_build(const PhaseArgs &a, int grid, cudaStream_t s);
+void launch_sweep(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
+int sweep_occupancy();
 int scan_occupancy();
 int eval_occupancy();
 constexpr int CAND_SLACK_PER_WARP = 64;  // chunked reservations: unused tail per scanning warp

@@ -416,6 +416,359 @@ __global__ void __launch_bounds__(K4B_THREADS, K4B_MIN_BLOCKS) k_eval(const Phas
   }
 }
 
+// ------------------------------------------------------------------ boundary sets
+// bset word (t, c, pr), t = sweep tile (img, ty, tx) of TX x TY blocks, c = cx + 2 cy the phase
+// colour, pr = plane row 0..TY/2-1: bit i <-> block (tx*TX + 2i + cx, ty*TY + 2pr + cy).
+// Invariant before every phase: each block that is a boundary block (Eq. 2) whose label can
+// pass the static gate (active[A] for CLASS/BSP, anything otherwise) has its bit set.  Set
+// bits may be stale (the sweep re-tests everything and clears them).
+static_assert(TX == 64 && TY == 16, "bset layout assumes 64 x 16 sweep tiles");
+constexpr int BSET_WORDS_PER_TILE = 4 * (TY / 2);  // 32
+
+__device__ __forceinline__ uint32_t bset_word(const StageDev &st, int img, int gx, int gy) {
+  const uint32_t t = ((uint32_t)img * (uint32_t)st.tiles_y + (uint32_t)(gy >> 4)) * (uint32_t)st.tiles_x +
+                     (uint32_t)(gx >> 6);
+  return t * BSET_WORDS_PER_TILE + (uint32_t)(((gx & 1) | ((gy & 1) << 1)) * (TY / 2) + ((gy & 15) >> 1));
+}
+__device__ __forceinline__ void bset_set(uint32_t *bset, const StageDev &st, int img, int gx, int gy) {
+  atomicOr(&bset[bset_word(st, img, gx, gy)], 1u << ((gx & 63) >> 1));
+}
+// the neighbours that a committed move p: A -> B turns into boundary blocks (4-bit mask over
+// N, E, S, W): label != B, inside the image, and passing the static gate
+__device__ __forceinline__ void bset_insert(uint32_t *bset, const StageDev &st, int img, int gx, int gy,
+                                            unsigned ins) {
+  if (ins & 1u) bset_set(bset, st, img, gx, gy - 1);
+  if (ins & 2u) bset_set(bset, st, img, gx + 1, gy);
+  if (ins & 4u) bset_set(bset, st, img, gx, gy + 1);
+  if (ins & 8u) bset_set(bset, st, img, gx - 1, gy);
+}
+
+// position of the r-th set bit (0-based) of w; r < popc(w)
+__device__ __forceinline__ unsigned nth_set_bit(uint32_t w, unsigned r) {
+  unsigned pos = 0;
+#pragma unroll
+  for (int h = 16; h > 0; h >>= 1) {
+    const unsigned lo = __popc(w & ((1u << h) - 1u));
+    if (r >= lo) {
+      r -= lo;
+      pos += h;
+      w >>= h;
+    }
+  }
+  return pos;
+}
+
+// K4 build (once per stage, after the transition): one CTA per sweep tile, thread (r, q) owns
+// the 4 blocks gx0+4q .. gx0+4q+3 of row gy0+r; writes all 32 words of the tile.
+__global__ void __launch_bounds__(256) k_bset_build(const PhaseArgs a) {
+  const StageDev &st = a.st;
+  const int nbx = st.nbx, nby = st.nby;
+  const unsigned ntiles = a.worklist ? *a.nwork : (unsigned)(st.tiles_x * st.tiles_y) * (unsigned)a.B;
+  const int r = threadIdx.x >> 4, q = threadIdx.x & 15;
+  for (unsigned w = blockIdx.x; w < ntiles; w += gridDim.x) {
+    const uint32_t t = a.worklist ? (uint32_t)a.worklist[w] : w;
+    const uint32_t rr = fdiv(t, st.fd_tx), img = fdiv(rr, st.fd_ty);
+    const int gx0 = (int)(t - rr * (uint32_t)st.tiles_x) * TX, gy0 = (int)(rr - img * (uint32_t)st.tiles_y) * TY;
+    const int32_t *map = st.map + (size_t)img * nby * nbx;
+    const int gy = gy0 + r, x0 = gx0 + 4 * q;
+    const bool row_in = gy < nby;
+    int L[4], U[4], D[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int x = x0 + k;
+      const bool in = row_in && x < nbx;
+      const size_t o = (size_t)gy * nbx + x;
+      L[k] = in ? map[o] : -1;
+      U[k] = in && gy > 0 ? map[o - nbx] : -1;
+      D[k] = in && gy + 1 < nby ? map[o + nbx] : -1;
+    }
+    int left = __shfl_up_sync(FULL, L[3], 1, 16), right = __shfl_down_sync(FULL, L[0], 1, 16);
+    if (q == 0) left = (row_in && x0 > 0 && x0 - 1 < nbx) ? map[(size_t)gy * nbx + x0 - 1] : -1;
+    if (q == 15) right = (row_in && x0 + 4 < nbx) ? map[(size_t)gy * nbx + x0 + 4] : -1;
+    unsigned s = 0;
+    int last = -1;
+    bool last_act = false;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      const int A = L[k];
+      const int Wn = k ? L[k - 1] : left, En = k < 3 ? L[k + 1] : right;
+      bool b = A >= 0 && ((U[k] >= 0 && U[k] != A) | (D[k] >= 0 && D[k] != A) | (Wn >= 0 && Wn != A) |
+                          (En >= 0 && En != A));
+      if (b && a.gating == 1) {
+        if (A != last) {
+          last = A;
+          last_act = a.sp.active[(size_t)img * a.M + A] != 0;
+        }
+        b = last_act;
+      }
+      s |= (unsigned)b << k;
+    }
+    // colour cx = 0: columns 4q, 4q+2 -> bits 2q, 2q+1; cx = 1: columns 4q+1, 4q+3
+    unsigned w0 = ((s & 1u) | ((s >> 1) & 2u)) << (2 * q);
+    unsigned w1 = (((s >> 1) & 1u) | ((s >> 2) & 2u)) << (2 * q);
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+      w0 |= __shfl_xor_sync(FULL, w0, o);
+      w1 |= __shfl_xor_sync(FULL, w1, o);
+    }
+    if (q == 0) {
+      const int cy = r & 1;
+      uint32_t *tw = a.bset + (size_t)t * BSET_WORDS_PER_TILE + (r >> 1);
+      tw[(0 + 2 * cy) * (TY / 2)] = w0;
+      tw[(1 + 2 * cy) * (TY / 2)] = w1;
+    }
+  }
+}
+
+// K4 sweep (fused scan + evaluate, one launch per phase): warps stride over groups of 4 sweep
+// tiles; lane l loads bset word (tile l/8, colour c, plane row l%8), the set bits are
+// distributed 32 at a time over the lanes, and every lane re-tests its block from the label
+// map (boundary, static gate, simple point, Eq. 7), then evaluates Eqs. 1-3 as K4b does.
+template <bool PIXEL, bool GATED>
+__global__ void __launch_bounds__(K4B_THREADS, K4B_MIN_BLOCKS) k_sweep(const PhaseArgs a) {
+  if (sweep_skipped(a.prev)) return;
+  const int lane = lane_id();
+  const StageDev &st = a.st;
+  const int nbx = st.nbx, nby = st.nby;
+  const unsigned ntiles = a.worklist ? *a.nwork : (unsigned)(st.tiles_x * st.tiles_y) * (unsigned)a.B;
+  const unsigned G = (unsigned)a.gwords;  // words per warp iteration (4..32, power of 2)
+  const unsigned ngroups = (ntiles * (TY / 2) + G - 1) / G;
+  const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const int colour = a.cx | (a.cy << 1);
+  unsigned c_cand = 0, c_topo = 0, c_prop = 0, c_srej = 0, c_commit = 0;
+  unsigned long long pbase = 0;  // this warp's reserved proposal slots
+  int pleft = 0;
+  for (unsigned g = gw; g < ngroups; g += nw) {
+    // ---- this lane's word
+    const unsigned q = g * G + (unsigned)lane, w = q >> 3;  // (tile slot, plane row q % 8)
+    uint32_t word = 0, wpos = 0, widx = 0;
+    int wimg = 0;
+    if ((unsigned)lane < G && w < ntiles) {
+      const uint32_t t = a.worklist ? (uint32_t)a.worklist[w] : w;
+      const uint32_t rr = fdiv(t, st.fd_tx), img = fdiv(rr, st.fd_ty);
+      const int gx0 = (int)(t - rr * (uint32_t)st.tiles_x) * TX, gy0 = (int)(rr - img * (uint32_t)st.tiles_y) * TY;
+      widx = t * BSET_WORDS_PER_TILE + (uint32_t)(colour * (TY / 2) + (q & 7));
+      word = a.bset[widx];
+      wpos = (uint32_t)(gx0 + a.cx) | ((uint32_t)(gy0 + 2 * (q & 7) + a.cy) << 16);
+      wimg = (int)img;
+    }
+    const unsigned cw = __popc(word);
+    unsigned incl = cw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const unsigned total = __shfl_sync(FULL, incl, 31);
+    for (unsigned rb = 0; rb < total; rb += 32) {
+      const unsigned k = rb + lane;
+      int j = 0;  // the lane whose word holds candidate k: #lanes with incl <= k
+#pragma unroll
+      for (int h = 16; h > 0; h >>= 1) {
+        const unsigned v = __shfl_sync(FULL, incl, j + h - 1);
+        if (v <= k) j += h;
+      }
+      const uint32_t wj = __shfl_sync(FULL, word, j);
+      const unsigned ej = __shfl_sync(FULL, incl, j) - __popc(wj);
+      const uint32_t pj = __shfl_sync(FULL, wpos, j);
+      const uint32_t xj = __shfl_sync(FULL, widx, j);
+      const int img = __shfl_sync(FULL, wimg, j);
+      const bool have = k < total;
+      bool cand = false, emit = false, prop = false, srej = false;
+      int A = 0, Bm = 0, kb = img * a.M, gx = 0, gy = 0;
+      unsigned ins = 0;
+      uint32_t rgb = 0;
+      long long d[6] = {0, 0, 0, 0, 0, 0};
+      if (have) {
+        const unsigned bit = nth_set_bit(wj, k - ej);
+        gx = (int)(pj & 0xffffu) + 2 * (int)bit;
+        gy = (int)(pj >> 16);
+        const int32_t *m = st.map + (size_t)img * nby * nbx;
+        const size_t o = (size_t)gy * nbx + gx;
+        const bool hN = gy > 0, hS = gy + 1 < nby, hW = gx > 0, hE = gx + 1 < nbx;
+        A = m[o];
+        const int nq0 = hN ? m[o - nbx] : -1, nq1 = hE ? m[o + 1] : -1;
+        const int nq2 = hS ? m[o + nbx] : -1, nq3 = hW ? m[o - 1] : -1;
+        const int dNE = hN && hE ? m[o - nbx + 1] : -1, dSE = hS && hE ? m[o + nbx + 1] : -1;
+        const int dSW = hS && hW ? m[o + nbx - 1] : -1, dNW = hN && hW ? m[o - nbx - 1] : -1;
+        const int nq[4] = {nq0, nq1, nq2, nq3};
+        const bool bnd = (nq0 >= 0 && nq0 != A) | (nq1 >= 0 && nq1 != A) | (nq2 >= 0 && nq2 != A) |
+                         (nq3 >= 0 && nq3 != A);
+        bool keep = bnd;
+        Rec recA;
+        if (bnd) {
+          recA = a.sp.rec[kb + A];
+          if (a.gating == 1) keep = ((recA.cq2f >> 16) & F_ACTIVE) != 0u;
+        }
+        if (!keep) {
+          atomicAnd(&a.bset[xj], ~(1u << bit));  // stale: no longer a gated boundary block
+        } else {
+          const unsigned m8 = (unsigned)(nq0 == A) | ((unsigned)(dNE == A) << 1) | ((unsigned)(nq1 == A) << 2) |
+                              ((unsigned)(dSE == A) << 3) | ((unsigned)(nq2 == A) << 4) |
+                              ((unsigned)(dSW == A) << 5) | ((unsigned)(nq3 == A) << 6) |
+                              ((unsigned)(dNW == A) << 7);
+          const bool topo_ok = simple_point(m8);
+          // distinct candidate labels (A8), compacted: cb[0..nb) with the slot mask cm of each;
+          // maskA = slots labelled A.  Records: first 16 B (means + flags).
+          int cb[4] = {0, 0, 0, 0};
+          unsigned cm[4] = {0u, 0u, 0u, 0u};
+          unsigned maskA = 0;
+          int nb = 0;
+#pragma unroll
+          for (int s = 0; s < 4; s++) {
+            const int L = nq[s];
+            if (L == A) maskA |= 1u << s;
+            if (L < 0 || L == A) continue;
+            bool found = false;
+#pragma unroll
+            for (int r = 0; r < s; r++)
+              if (r < nb && cb[r] == L) {
+                cm[r] |= 1u << s;
+                found = true;
+              }
+            if (!found) {
+#pragma unroll
+              for (int r = 0; r <= s; r++)
+                if (r == nb) {
+                  cb[r] = L;
+                  cm[r] = 1u << s;
+                }
+              nb++;
+            }
+          }
+          int4 rn[4];
+          const bool need_rn = topo_ok || a.gating == 2;
+#pragma unroll
+          for (int k = 0; k < 4; k++)
+            rn[k] = (need_rn && k < nb) ? __ldg(reinterpret_cast<const int4 *>(&a.sp.rec[kb + cb[k]]))
+                                        : make_int4(0, 0, 0, 0);
+          cand = true;
+          if (a.gating == 2) {  // Eq. 7: a neighbour of another label and another class
+            const unsigned yA = (recA.cq2f >> 18) & 3u;
+            bool e7 = false;
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+              if (k < nb) e7 |= ((((unsigned)rn[k].w >> 18) & 3u) != yA);
+            cand = e7;
+          }
+          emit = cand && topo_ok;
+          if (emit) {
+            long long bw = 1, bh = 1;  // E_b edge weights: W/E edges have length bh, N/S edges bw
+            if (PIXEL) {
+              const uint8_t *p = a.image + (((size_t)img * a.H + gy) * a.W + gx) * 3;
+              const uint32_t r = p[0], g2 = p[1], b = p[2];
+              rgb = r | (g2 << 8) | (b << 16);
+              d[0] = 1; d[1] = r; d[2] = g2; d[3] = b; d[4] = gx; d[5] = gy;
+            } else {
+              block_data_blk(st, img, gx, gy, d);
+              bw = st.xs[gx + 1] - st.xs[gx];
+              bh = st.ys[gy + 1] - st.ys[gy];
+            }
+            // weight of the slots in mask m: N (1), S (4) edges have length bw; E (2), W (8) bh
+            auto wsum = [&](unsigned m) -> long long {
+              return PIXEL ? (long long)__popc(m) : bw * __popc(m & 5u) + bh * __popc(m & 10u);
+            };
+            const long long wA = wsum(maskA);
+            const long long n = d[0];
+            const long long cA0 = recA.cq01 & 0xffffu, cA1 = recA.cq01 >> 16, cA2 = recA.cq2f & 0xffffu;
+            const long long mA0 = recA.mux, mA1 = recA.muy;
+            const long long S0 = d[1] << (FRAC + 1), S1 = d[2] << (FRAC + 1), S2 = d[3] << (FRAC + 1);
+            const long long P0 = d[4] << (FRAC + 1), P1 = d[5] << (FRAC + 1);
+            bool hv = false;
+            i128 bestE = 0;
+            int bestB = 0;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+              if (k >= nb) break;
+              const int B = cb[k];
+              // Eq. 1 difference of relabelling the block A -> B under the frozen means (x 2^-16
+              // of the oracle's weighted dE): X = colour part + E_b part (int64, exact),
+              // dP = position part; E = X * 2^16 + lambda_pos * dP (128-bit)
+              const long long cB0 = (unsigned)rn[k].z & 0xffffu, cB1 = (unsigned)rn[k].z >> 16;
+              const long long cB2 = (unsigned)rn[k].w & 0xffffu;
+              const long long dB2 = 2 * (wA - wsum(cm[k]));
+              const long long X = (cB0 - cA0) * (n * (cB0 + cA0) - S0) + (cB1 - cA1) * (n * (cB1 + cA1) - S1) +
+                                  (cB2 - cA2) * (n * (cB2 + cA2) - S2) + a.lam_b * dB2;
+              const long long mB0 = rn[k].x, mB1 = rn[k].y;
+              const long long dP = (mB0 - mA0) * (n * (mB0 + mA0) - P0) + (mB1 - mA1) * (n * (mB1 + mA1) - P1);
+              const unsigned long long plo = (unsigned long long)a.lam_pos * (unsigned long long)dP;
+              const long long phi = __mul64hi(a.lam_pos, dP);
+              const i128 E = ((i128)X << 16) + (i128)(((unsigned __int128)(unsigned long long)phi << 64) | plo);
+              if (!hv || E < bestE || (E == bestE && B < bestB)) {
+                hv = true;
+                bestE = E;
+                bestB = B;
+              }
+            }
+            if (hv && bestE < 0) {
+              if (GATED && ((long long)recA.n - d[0]) * a.l_den < a.l_num * (long long)recA.init) {
+                srej = true;  // A12: the desired move would leave A below l * InitSize
+                if (a.size_mode == 2) {
+                  a.sp.victim[kb + A] = 1;
+                  *a.victim_any = 1u;
+                }
+              } else {
+                prop = true;
+                Bm = bestB;
+                // neighbours that become boundary blocks if the move commits: label != B and
+                // passing the static gate (A passed it; others from their record flags)
+                ins = maskA;
+#pragma unroll
+                for (int k = 0; k < 4; k++)
+                  if (k < nb && cb[k] != Bm && (a.gating != 1 || (((unsigned)rn[k].w >> 16) & F_ACTIVE)))
+                    ins |= cm[k];
+              }
+            }
+          }
+        }
+      }
+      c_cand += __popc(__ballot_sync(FULL, cand));
+      c_topo += __popc(__ballot_sync(FULL, emit));
+      c_srej += __popc(__ballot_sync(FULL, srej));
+      const unsigned pm = __ballot_sync(FULL, prop);
+      c_prop += __popc(pm);
+      if (pm) {
+        const size_t idx = ((size_t)img * nby + gy) * nbx + gx;
+        if (!GATED) {  // size_mode NONE: no budget to check, commit in place
+          if (prop) {
+            st.map[idx] = Bm;
+            bset_insert(a.bset, st, img, gx, gy, ins);
+          }
+          agg_sums(prop, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp);
+          agg_sums(prop, kb + Bm, d, false, a.sp.sums, a.sp.dirty, a.stamp);
+          c_commit += __popc(pm);
+        } else {
+          agg_add_i32(prop, kb + A, (int)d[0], a.sp.out);
+          const int np = __popc(pm);
+          if (np > pleft) {  // retire the rest of the chunk (sentinels), reserve a new one
+            if (lane < pleft) a.props[pbase + lane] = make_uint4(0u, 0xffffffffu, 0u, 0u);
+            unsigned long long nb = 0;
+            if (lane == 0) nb = atomicAdd(a.prop_count, (unsigned long long)CHUNK);
+            pbase = __shfl_sync(FULL, nb, 0);
+            pleft = CHUNK;
+          }
+          if (prop)
+            a.props[pbase + __popc(pm & lanemask_lt())] =
+                make_uint4((unsigned)idx, (unsigned)A, (unsigned)Bm, rgb | (ins << 24));
+          pbase += np;
+          pleft -= np;
+        }
+      }
+    }
+  }
+  if (GATED) {
+    if (lane < pleft) a.props[pbase + lane] = make_uint4(0u, 0xffffffffu, 0u, 0u);
+    if (lane + 32 < pleft) a.props[pbase + lane + 32] = make_uint4(0u, 0xffffffffu, 0u, 0u);
+  }
+  if (lane == 0) {
+    if (c_cand) atomicAdd(&a.cnt[0], (unsigned long long)c_cand);
+    if (c_topo) atomicAdd(&a.cnt[1], (unsigned long long)c_topo);
+    if (c_prop) atomicAdd(&a.cnt[2], (unsigned long long)c_prop);
+    if (c_srej) atomicAdd(&a.cnt[3], (unsigned long long)c_srej);
+    if (c_commit) atomicAdd(&a.cnt[4], (unsigned long long)c_commit);
+  }
+}
+
 // ------------------------------------------------------------------ K5: commit
 template <bool PIXEL>
 __global__ void __launch_bounds__(256) k_commit(const PhaseArgs a) {
@@ -449,6 +802,7 @@ __global__ void __launch_bounds__(256) k_commit(const PhaseArgs a) {
           block_data_blk(a.st, img, gx, gy, d);
         }
         a.st.map[idx] = B;
+        if (a.bset) bset_insert(a.bset, a.st, img, gx, gy, pr.w >> 24);
       } else {
         rej = true;
         if (a.size_mode == 2) {
@@ -515,6 +869,24 @@ void launch_eval(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
   else if (pixel) k_eval<true, false><<<grid, K4B_THREADS, 0, s>>>(a);
   else if (gated) k_eval<false, true><<<grid, K4B_THREADS, 0, s>>>(a);
   else k_eval<false, false><<<grid, K4B_THREADS, 0, s>>>(a);
+}
+
+int sweep_occupancy() {
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sweep<true, true>, K4B_THREADS, 0);
+  return nb < 1 ? 1 : nb;
+}
+
+void launch_bset_build(const PhaseArgs &a, int grid, cudaStream_t s) {
+  k_bset_build<<<grid, 256, 0, s>>>(a);
+}
+
+void launch_sweep(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
+  const bool gated = a.size_mode != 0;
+  if (pixel && gated) k_sweep<true, true><<<grid, K4B_THREADS, 0, s>>>(a);
+  else if (pixel) k_sweep<true, false><<<grid, K4B_THREADS, 0, s>>>(a);
+  else if (gated) k_sweep<false, true><<<grid, K4B_THREADS, 0, s>>>(a);
+  else k_sweep<false, false><<<grid, K4B_THREADS, 0, s>>>(a);
 }
 
 void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {

@@ -221,16 +221,15 @@ def run_ours(args):
         r.segment(img, p, labels)
     torch.cuda.synchronize()
 
-    # timed region: K segmentations, events on the launching stream; profiling events on
-    r.set_profiling(1)
+    # timed region 1 (the value): K segmentations (one CUDA-graph launch each), CUDA events on
+    # the launching stream, no per-kernel events inside
+    r.set_profiling(0)
+    r.segment(img, p, labels)  # capture + instantiate the graph outside the timed region
     clocks = Clocks(local) if rank == 0 else None
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    prof_ms = np.zeros((rb.NK, rb.MAX_STAGES))
-    prof_launch = np.zeros((rb.NK, rb.MAX_STAGES))
-    total_launches = 0
     ev0.record(stream)
     for _ in range(args.steps):
         r.segment(img, p, labels)
@@ -240,10 +239,18 @@ def run_ours(args):
         dist.barrier()
     dev_ms = ev0.elapsed_time(ev1)
     ck = clocks.stop() if clocks else None
-    # per-kernel profile of the timed steps (profile() reports the last segmentation)
-    pr = r.profile()
-    prof_ms += pr.ms_array()
-    prof_launch += pr.launch_array()
+    # timed region 2 (the per-kernel breakdown and the roofline): the same K segmentations with
+    # CUDA events around every launch group, on the launching stream, live
+    r.set_profiling(1)
+    r.segment(img, p, labels)
+    torch.cuda.synchronize()
+    prof_ms = np.zeros((rb.NK, rb.MAX_STAGES))
+    prof_launch = np.zeros((rb.NK, rb.MAX_STAGES))
+    for _ in range(args.steps):
+        r.segment(img, p, labels)
+        pr = r.profile()  # this segmentation's per-launch-group event times
+        prof_ms += pr.ms_array() / args.steps
+        prof_launch += pr.launch_array() / args.steps
     total_launches = int(pr.total_launches)
     _, info = r.stats(0)
 
@@ -285,37 +292,40 @@ def run_ours(args):
     if rank == 0:
         peak, peak_src = peaks()
         pb = phase_bytes(info, w, window)
-        # Dominant HBM kernel: the K4a scan at the pixel stage (the last stage).  Its algorithmic
-        # bytes per launch are the label reads of the phase's window: 4 B x window blocks
-        # (SURVEY §8(d)); colour reads and label writes belong to K4b/K5 and enter the phase-set
-        # figure below.
+        # Dominant kernel: the K4 sweep (k_sweep: boundary-set driven scan + evaluate) at the
+        # pixel stage (the last stage).  Algorithmic bytes per launch: the label
+        # reads of the phase's window, 4 B x window blocks, plus the colour reads of the
+        # topology-passing candidates, 3 B each.  Label writes (4 B x commits) belong to K5 and
+        # enter the phase-set figure below.
         ps = len(p.block_sizes) - 1
         runs = int(info.stage_sweeps_run[ps]) * 4
-        scan_bytes = 4 * window[ps] * runs
-        scan_ms = float(prof_ms[rb.K_PROPOSE][ps])
-        scan_launch = int(prof_launch[rb.K_PROPOSE][ps])
+        cnt = info.counters()
+        topo_ps = sum(int(cnt[ps, t, ph, rb.C_TOPO]) for t in range(int(info.stage_sweeps_run[ps])) for ph in range(4))
+        sweep_bytes = 4 * window[ps] * runs + 3 * topo_ps
+        sweep_ms = float(prof_ms[rb.K_PROPOSE][ps])
+        sweep_launch = int(prof_launch[rb.K_PROPOSE][ps])
         steps_ms = float(prof_ms[[rb.K_PYRAMID, rb.K_SNAPSHOT, rb.K_PROPOSE, rb.K_COMMIT, rb.K_MERGE, rb.K_PREDICT,
                                   rb.K_TRANSITION, rb.K_FINAL, rb.K_EVAL]].sum())
-        achieved = scan_bytes / (scan_ms / 1e3) / 1e9 if scan_ms > 0 else 0.0
+        achieved = sweep_bytes / (sweep_ms / 1e3) / 1e9 if sweep_ms > 0 else 0.0
         traffic = None
-        tfile = os.path.join(ROOT, "profiles", "scan_traffic.json")
-        if os.path.exists(tfile):  # ncu dram bytes of one pixel-stage k_scan launch (committed capture)
+        tfile = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+        if os.path.exists(tfile):  # ncu dram bytes of one pixel-stage k_sweep launch (committed capture)
             with open(tfile) as f:
                 traffic = json.load(f).get("dram_bytes_per_launch")
         all_bytes = sum(v[0] for v in pb.values())
         phase_ms = float(prof_ms[rb.K_PHASESET].sum())
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": f"k_scan (K4a, TMA-streamed parity-phase scan), pixel stage ({scan_launch} launches/step)",
-                "bytes_per_launch": round(scan_bytes / max(1, scan_launch)),
-                "avg_launch_ms": round(scan_ms / max(1, scan_launch), 4),
-                "share_of_step": round(scan_ms / max(1e-9, steps_ms), 4), "peak_source": peak_src,
-                "bytes_model": "4 B x blocks within Chebyshev distance 1 of a block with an active label, per phase",
-                "all_stages_scan_GBps": round(sum(4 * window[s] * int(info.stage_sweeps_run[s]) * 4
-                                                  for s in range(ps + 1)) /
-                                              (float(prof_ms[rb.K_PROPOSE].sum()) / 1e3) / 1e9, 1),
+                "kernel": f"k_sweep (K4: boundary-set driven scan + evaluate), pixel stage ({sweep_launch} launches/step)",
+                "bytes_per_launch": round(sweep_bytes / max(1, sweep_launch)),
+                "avg_launch_ms": round(sweep_ms / max(1, sweep_launch), 4),
+                "share_of_step": round(sweep_ms / max(1e-9, steps_ms), 4), "peak_source": peak_src,
+                "bytes_model": "4 B x blocks within Chebyshev distance 1 of a block with an active label "
+                               "+ 3 B x topology-passing candidates, per phase",
                 "phase_set": {"GBps": round(all_bytes / (phase_ms / 1e3) / 1e9, 1) if phase_ms > 0 else None,
-                              "kernels": "snapshot + K4a scan + K4b eval + K5 commit, all stages",
+                              "frac": round(all_bytes / (phase_ms / 1e3) / 1e9 / peak, 4) if phase_ms > 0 else None,
+                              "ms_per_step": round(phase_ms, 3),
+                              "kernels": "K3 snapshot + K4 sweep + K5 commit, all stages",
                               "bytes_model": "4 B x window + c_s x topology-passing candidates + 4 B x commits"}}
         line = {"metric": METRIC, "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
@@ -325,10 +335,9 @@ def run_ours(args):
                 "roofline": roof, "e2e": e2e, "gpu_launches": total_launches * args.steps,
                 "clocks": ck,
                 "per_kernel_ms_per_step": {nm: round(float(prof_ms[k].sum()), 3) for k, nm in enumerate(
-                    ["pyramid", "snapshot", "scan", "commit", "merge", "predict", "transition", "final",
+                    ["pyramid", "snapshot", "sweep", "commit", "merge", "predict", "transition", "final",
                      "phase_set", "eval"])},
-                "stage_scan_ms": [round(float(x), 3) for x in prof_ms[rb.K_PROPOSE][:len(p.block_sizes)]],
-                "stage_eval_ms": [round(float(x), 3) for x in prof_ms[rb.K_EVAL][:len(p.block_sizes)]],
+                "stage_sweep_ms": [round(float(x), 3) for x in prof_ms[rb.K_PROPOSE][:len(p.block_sizes)]],
                 "stage_sweeps_run": [int(x) for x in info.stage_sweeps_run[:len(p.block_sizes)]],
                 "alive": int(info.alive), "active": int(info.active)}
         if not args.no_cpu:

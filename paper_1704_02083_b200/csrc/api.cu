@@ -97,6 +97,19 @@ struct rapid_ctx {
   // occupancy
   int scan_grid = 0, eval_grid = 0, sweep_grid = 0;  // persistent grid sizes (CTAs)
   bool use_bset = true;  // RAPID_SWEEP=scan selects the full-scan path K4a + K4b (A/B testing)
+  // CUDA graph of the whole segmentation (one launch per call): captured on a private stream,
+  // replayed while the key (buffers, geometry, params, profiling level, plan) is unchanged
+  bool use_graph = true;  // RAPID_NO_GRAPH=1 enqueues the kernels one by one (A/B testing)
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  unsigned plan_gen = 0;
+  struct GraphKey {
+    const void *image;
+    const void *labels;
+    int H, W, prof;
+    unsigned plan_gen;
+    rapid_params p;
+  } gkey;
   bool use_tma = true;  // RAPID_NO_TMA=1 forces the LDG tile loader (A/B testing)
   // profiling
   int prof = 0;  // 0 off, 1 events, 2 events + window counting
@@ -346,6 +359,7 @@ int build_plan(rapid_ctx *c, int H, int W, const rapid_params *p) {
   if ((rc = cuda_check(c, e, "upload tables"))) return rc;
   N.valid = true;
   c->plan = std::move(N);
+  c->plan_gen++;  // buffers may have moved: a captured graph is stale
   return RAPID_OK;
 }
 
@@ -398,7 +412,13 @@ struct Timer {  // CUDA events around a launch group (profiling mode only)
   Timer(rapid_ctx *c_, cudaStream_t s_, int cls_, int stage_) : c(c_), s(s_), cls(cls_), stage(stage_) {
     if (!c->prof) return;
     a = next();
-    cudaEventRecord(a, s);
+    record(a);
+  }
+  void record(cudaEvent_t e) {  // inside a captured graph: an external (real, timeable) record
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    else cudaEventRecord(e, s);
   }
   cudaEvent_t next() {
     if (c->ev_used == c->ev_pool.size()) {
@@ -411,7 +431,7 @@ struct Timer {  // CUDA events around a launch group (profiling mode only)
   ~Timer() {
     if (!c->prof) return;
     cudaEvent_t b = next();
-    cudaEventRecord(b, s);
+    record(b);
     c->evs.push_back({cls, stage, a, b});
   }
 };
@@ -430,6 +450,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
   c->stopped = false;
   c->stop_map = nullptr;
   cudaMemsetAsync(ctl, 0, sizeof(Ctl), s);
+  // dirty stamps restart every call (stamps are call-invariant, so a captured graph replays)
+  cudaMemsetAsync(c->dirty, 0, sizeof(uint32_t) * K, s);
 
   StageDev sd[MAXS];
   struct alignas(64) TMap {
@@ -730,6 +752,8 @@ void rapid_free(rapid_ctx *c) {
   cudaGetDevice(&prev);
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   void *ptrs[] = {c->sums, c->rc, c->rec, c->init, c->out, c->remap, c->head,
                   c->vlist, c->alist, c->pairs, c->alive, c->active, c->victim, c->y, c->dirty,
                   c->deg, c->chunk, c->hkeys, c->candE, c->hvals, c->hnext, c->candT, c->ctl,
@@ -768,7 +792,7 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
       (rc = dalloc(c, &c->head, K)) || (rc = dalloc(c, &c->vlist, K)) || (rc = dalloc(c, &c->alist, K)) ||
       (rc = dalloc(c, &c->pairs, 2 * K)) || (rc = dalloc(c, &c->alive, K)) ||
       (rc = dalloc(c, &c->active, K)) || (rc = dalloc(c, &c->victim, K)) || (rc = dalloc(c, &c->y, K)) ||
-      (rc = dalloc(c, &c->dirty, K)) || (rc = dalloc(c, &c->deg, K + 1)) ||
+      (rc = dalloc(c, &c->dirty, K + 4)) || (rc = dalloc(c, &c->deg, K + 1)) ||
       (rc = dalloc(c, &c->chunk, K / 1024 + 2)) || (rc = dalloc(c, &c->hkeys, hc)) ||
       (rc = dalloc(c, &c->hvals, hc)) || (rc = dalloc(c, &c->hnext, hc)) ||
       (rc = dalloc(c, &c->candT, hc)) || (rc = dalloc(c, &c->candE, 2 * hc)) ||
@@ -794,6 +818,10 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
     const char *e = getenv("RAPID_NO_TMA");
     c->use_tma = !(e && e[0] == '1');
   }
+  {
+    const char *e = getenv("RAPID_NO_GRAPH");
+    c->use_graph = !(e && e[0] == '1');
+  }
   rc = cuda_check(c, cudaDeviceSynchronize(), "rapid_init");
   if (rc) {
     rapid_free(c);
@@ -815,8 +843,47 @@ int rapid_segment(rapid_ctx *c, const uint8_t *image, int32_t H, int32_t W, cons
   if ((rc = build_plan(c, H, W, p))) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   cudaGetLastError();
-  rc = enqueue(c, image, H, W, p, labels_out, s);
-  c->stamp_base += (uint32_t)(p->n_stages * p->sweeps * 4 + 8);
+  if (c->use_graph && c->stop_kind == 0) {
+    rapid_ctx::GraphKey k;
+    memset(&k, 0, sizeof k);
+    k.image = image;
+    k.labels = labels_out;
+    k.H = H;
+    k.W = W;
+    k.prof = c->prof;
+    k.plan_gen = c->plan_gen;
+    k.p = *p;
+    if (!c->gexec || memcmp(&k, &c->gkey, sizeof k) != 0) {
+      if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+      }
+      if (!c->cap_stream && (rc = cuda_check(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking),
+                                             "capture stream")))
+        return rc;
+      if ((rc = cuda_check(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal),
+                           "begin capture")))
+        return rc;
+      rc = enqueue(c, image, H, W, p, labels_out, c->cap_stream);
+      cudaGraph_t g = nullptr;
+      const cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g);
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if ((rc = cuda_check(c, e, "end capture"))) return rc;
+      const cudaError_t ei = cudaGraphInstantiate(&c->gexec, g, 0);
+      cudaGraphDestroy(g);
+      if ((rc = cuda_check(c, ei, "graph instantiate"))) {
+        c->gexec = nullptr;
+        return rc;
+      }
+      c->gkey = k;
+    }
+    rc = cuda_check(c, cudaGraphLaunch(c->gexec, s), "graph launch");
+  } else {
+    rc = enqueue(c, image, H, W, p, labels_out, s);
+  }
   c->last = *p;
   c->last_prof = c->prof;
   c->have_run = true;
@@ -941,11 +1008,12 @@ int rapid_get_profile(rapid_ctx *c, rapid_profile *out) {
   memset(out, 0, sizeof(*out));
   for (const ProfEv &e : c->evs) {
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, e.a, e.b);
+    if (cudaEventElapsedTime(&ms, e.a, e.b) != cudaSuccess) ms = 0.f;
     out->launches[e.cls][e.stage]++;
     out->ms[e.cls][e.stage] += ms;
   }
   out->total_launches = (uint64_t)c->launches;
+  cudaGetLastError();  // elapsed-time failures are not sticky; do not leak them into later calls
   return RAPID_OK;
 }
 

@@ -178,9 +178,16 @@ __device__ __forceinline__ void make_rec(const SpDev &sp, int k) {
 }
 
 __global__ void k_snapshot(const SnapArgs a) {
-  // full refresh (stamp 0) or only the superpixels stamped dirty by the previous phase
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.K; i += gridDim.x * blockDim.x)
-    if (a.stamp == 0u || a.sp.dirty[i] == a.stamp) make_rec(a.sp, i);
+  // full refresh (stamp 0) or only the superpixels stamped dirty by the previous phase; four
+  // stamps per thread (one 16-B load; the stamp array is padded to a multiple of 4)
+  const int n4 = (a.K + 3) >> 2;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+    const uint4 s4 = a.stamp ? *reinterpret_cast<const uint4 *>(a.sp.dirty + 4 * (size_t)i) : make_uint4(0, 0, 0, 0);
+    const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+      if (4 * i + j < a.K && (a.stamp == 0u || sv[j] == a.stamp)) make_rec(a.sp, 4 * i + j);
+  }
 }
 
 
@@ -810,7 +817,9 @@ void launch_stats0(const InitArgs &a, cudaStream_t s) {
 }
 
 void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s) {
-  k_snapshot<<<grid, 256, 0, s>>>(a);
+  // one pass: every thread checks 4 stamps once (grid capped at `grid` x 2)
+  const int g = grid_for(((size_t)a.K + 3) / 4, 256, 2 * grid);
+  k_snapshot<<<g, 256, 0, s>>>(a);
 }
 
 void launch_merge_round(const MergeArgs &a, int grid, cudaStream_t s, int *nlaunch) {

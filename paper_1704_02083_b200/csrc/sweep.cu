@@ -22,6 +22,7 @@
 //      warp-aggregated stats deltas.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -520,12 +521,48 @@ __global__ void __launch_bounds__(256) k_bset_build(const PhaseArgs a) {
   }
 }
 
+// lam * v exactly, for 0 <= lam < 2^31 and any int64 v: two 32 x 32 -> 64 products
+__device__ __forceinline__ i128 mul_u31_s64(long long lam, long long v) {
+  const unsigned long long p0 = (unsigned long long)(uint32_t)lam * (uint32_t)v;  // IMAD.WIDE.U32
+  const long long p1 = (long long)(int32_t)lam * (int32_t)(v >> 32);               // IMAD.WIDE
+  return ((i128)p1 << 32) + (i128)p0;
+}
+
+// 2^(-16) x the oracle's weighted dE of relabelling the block (data d) from A to the label of
+// record rb: E = X * 2^16 + lam_pos * dP with X = colour part + lam_b * dB2 (exact in int64)
+// and dP the position part (exact in int64).  At the pixel stage (n = 1, values
+// < 2^8, coordinates < 2^16) every factor fits 32 bits, so each product is one IMAD.WIDE.
+template <bool PIXEL>
+__device__ __forceinline__ i128 energy(const Rec &ra, const int4 rb, const long long d[6], long long dB2,
+                                       long long lam_pos, long long lam_b) {
+  const int cA0 = (int)(ra.cq01 & 0xffffu), cA1 = (int)(ra.cq01 >> 16), cA2 = (int)(ra.cq2f & 0xffffu);
+  const int cB0 = (int)((unsigned)rb.z & 0xffffu), cB1 = (int)((unsigned)rb.z >> 16);
+  const int cB2 = (int)((unsigned)rb.w & 0xffffu);
+  long long X, dP;
+  if (PIXEL) {
+    X = (long long)(cB0 - cA0) * (int)(cB0 + cA0 - ((int)d[1] << (FRAC + 1))) +
+        (long long)(cB1 - cA1) * (int)(cB1 + cA1 - ((int)d[2] << (FRAC + 1))) +
+        (long long)(cB2 - cA2) * (int)(cB2 + cA2 - ((int)d[3] << (FRAC + 1))) +
+        (long long)(int)lam_b * (int)dB2;
+    dP = (long long)(rb.x - ra.mux) * (int)(rb.x + ra.mux - ((int)d[4] << (FRAC + 1))) +
+         (long long)(rb.y - ra.muy) * (int)(rb.y + ra.muy - ((int)d[5] << (FRAC + 1)));
+  } else {
+    const long long n = d[0];
+    X = (long long)(cB0 - cA0) * (n * (cB0 + cA0) - (d[1] << (FRAC + 1))) +
+        (long long)(cB1 - cA1) * (n * (cB1 + cA1) - (d[2] << (FRAC + 1))) +
+        (long long)(cB2 - cA2) * (n * (cB2 + cA2) - (d[3] << (FRAC + 1))) + lam_b * dB2;
+    dP = (long long)(rb.x - ra.mux) * (n * ((long long)rb.x + ra.mux) - (d[4] << (FRAC + 1))) +
+         (long long)(rb.y - ra.muy) * (n * ((long long)rb.y + ra.muy) - (d[5] << (FRAC + 1)));
+  }
+  return ((i128)X << 16) + mul_u31_s64(lam_pos, dP);
+}
+
 // K4 sweep (fused scan + evaluate, one launch per phase): warps stride over groups of 4 sweep
 // tiles; lane l loads bset word (tile l/8, colour c, plane row l%8), the set bits are
 // distributed 32 at a time over the lanes, and every lane re-tests its block from the label
 // map (boundary, static gate, simple point, Eq. 7), then evaluates Eqs. 1-3 as K4b does.
-template <bool PIXEL, bool GATED>
-__global__ void __launch_bounds__(K4B_THREADS, K4B_MIN_BLOCKS) k_sweep(const PhaseArgs a) {
+template <bool PIXEL, bool GATED, int MINB>
+__global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) {
   if (sweep_skipped(a.prev)) return;
   const int lane = lane_id();
   const StageDev &st = a.st;
@@ -583,14 +620,26 @@ __global__ void __launch_bounds__(K4B_THREADS, K4B_MIN_BLOCKS) k_sweep(const Pha
         const unsigned bit = nth_set_bit(wj, k - ej);
         gx = (int)(pj & 0xffffu) + 2 * (int)bit;
         gy = (int)(pj >> 16);
+        // block data depends on the position only: issued together with the window loads
+        uint64_t pk = 0;
+        int bx0 = 0, bx1 = 1, by0 = 0, by1 = 1;
+        if (PIXEL) {
+          const uint8_t *p = a.image + (((size_t)img * a.H + gy) * a.W + gx) * 3;
+          rgb = (uint32_t)__ldcs(p) | ((uint32_t)__ldcs(p + 1) << 8) | ((uint32_t)__ldcs(p + 2) << 16);
+        } else {
+          pk = __ldcs(reinterpret_cast<const unsigned long long *>(st.bsum) + ((size_t)img * nby + gy) * nbx + gx);
+          bx0 = st.xs[gx]; bx1 = st.xs[gx + 1];
+          by0 = st.ys[gy]; by1 = st.ys[gy + 1];
+        }
         const int32_t *m = st.map + (size_t)img * nby * nbx;
         const size_t o = (size_t)gy * nbx + gx;
         const bool hN = gy > 0, hS = gy + 1 < nby, hW = gx > 0, hE = gx + 1 < nbx;
-        A = m[o];
-        const int nq0 = hN ? m[o - nbx] : -1, nq1 = hE ? m[o + 1] : -1;
-        const int nq2 = hS ? m[o + nbx] : -1, nq3 = hW ? m[o - 1] : -1;
-        const int dNE = hN && hE ? m[o - nbx + 1] : -1, dSE = hS && hE ? m[o + nbx + 1] : -1;
-        const int dSW = hS && hW ? m[o + nbx - 1] : -1, dNW = hN && hW ? m[o - nbx - 1] : -1;
+        // streaming loads (evict-first): keep L2 for the per-superpixel tables
+        A = __ldcs(m + o);
+        const int nq0 = hN ? __ldcs(m + o - nbx) : -1, nq1 = hE ? __ldcs(m + o + 1) : -1;
+        const int nq2 = hS ? __ldcs(m + o + nbx) : -1, nq3 = hW ? __ldcs(m + o - 1) : -1;
+        const int dNE = hN && hE ? __ldcs(m + o - nbx + 1) : -1, dSE = hS && hE ? __ldcs(m + o + nbx + 1) : -1;
+        const int dSW = hS && hW ? __ldcs(m + o + nbx - 1) : -1, dNW = hN && hW ? __ldcs(m + o - nbx - 1) : -1;
         const int nq[4] = {nq0, nq1, nq2, nq3};
         const bool bnd = (nq0 >= 0 && nq0 != A) | (nq1 >= 0 && nq1 != A) | (nq2 >= 0 && nq2 != A) |
                          (nq3 >= 0 && nq3 != A);
@@ -639,61 +688,46 @@ __global__ void __launch_bounds__(K4B_THREADS, K4B_MIN_BLOCKS) k_sweep(const Pha
           int4 rn[4];
           const bool need_rn = topo_ok || a.gating == 2;
 #pragma unroll
-          for (int k = 0; k < 4; k++)
-            rn[k] = (need_rn && k < nb) ? __ldg(reinterpret_cast<const int4 *>(&a.sp.rec[kb + cb[k]]))
-                                        : make_int4(0, 0, 0, 0);
+          for (int k2 = 0; k2 < 4; k2++)
+            rn[k2] = (need_rn && k2 < nb) ? __ldg(reinterpret_cast<const int4 *>(&a.sp.rec[kb + cb[k2]]))
+                                          : make_int4(0, 0, 0, 0);
           cand = true;
           if (a.gating == 2) {  // Eq. 7: a neighbour of another label and another class
             const unsigned yA = (recA.cq2f >> 18) & 3u;
             bool e7 = false;
 #pragma unroll
-            for (int k = 0; k < 4; k++)
-              if (k < nb) e7 |= ((((unsigned)rn[k].w >> 18) & 3u) != yA);
+            for (int k2 = 0; k2 < 4; k2++)
+              if (k2 < nb) e7 |= ((((unsigned)rn[k2].w >> 18) & 3u) != yA);
             cand = e7;
           }
           emit = cand && topo_ok;
           if (emit) {
-            long long bw = 1, bh = 1;  // E_b edge weights: W/E edges have length bh, N/S edges bw
+            long long bw = 1, bh = 1;  // E_b edge weights: N/S edges have length bw, W/E bh
             if (PIXEL) {
-              const uint8_t *p = a.image + (((size_t)img * a.H + gy) * a.W + gx) * 3;
-              const uint32_t r = p[0], g2 = p[1], b = p[2];
-              rgb = r | (g2 << 8) | (b << 16);
-              d[0] = 1; d[1] = r; d[2] = g2; d[3] = b; d[4] = gx; d[5] = gy;
+              d[0] = 1; d[1] = rgb & 0xffu; d[2] = (rgb >> 8) & 0xffu; d[3] = rgb >> 16; d[4] = gx; d[5] = gy;
             } else {
-              block_data_blk(st, img, gx, gy, d);
-              bw = st.xs[gx + 1] - st.xs[gx];
-              bh = st.ys[gy + 1] - st.ys[gy];
+              bw = bx1 - bx0;
+              bh = by1 - by0;
+              d[0] = bw * bh;
+              d[1] = (long long)(pk & 0x1FFFFFull);
+              d[2] = (long long)((pk >> 21) & 0x1FFFFFull);
+              d[3] = (long long)(pk >> 42);
+              d[4] = bh * ((bw * (2 * (long long)bx0 + bw - 1)) / 2);
+              d[5] = bw * ((bh * (2 * (long long)by0 + bh - 1)) / 2);
             }
-            // weight of the slots in mask m: N (1), S (4) edges have length bw; E (2), W (8) bh
-            auto wsum = [&](unsigned m) -> long long {
-              return PIXEL ? (long long)__popc(m) : bw * __popc(m & 5u) + bh * __popc(m & 10u);
+            // weight of the slots in mask s: N (1), S (4) edges have length bw; E (2), W (8) bh
+            auto wsum = [&](unsigned msk) -> long long {
+              return PIXEL ? (long long)__popc(msk) : bw * __popc(msk & 5u) + bh * __popc(msk & 10u);
             };
             const long long wA = wsum(maskA);
-            const long long n = d[0];
-            const long long cA0 = recA.cq01 & 0xffffu, cA1 = recA.cq01 >> 16, cA2 = recA.cq2f & 0xffffu;
-            const long long mA0 = recA.mux, mA1 = recA.muy;
-            const long long S0 = d[1] << (FRAC + 1), S1 = d[2] << (FRAC + 1), S2 = d[3] << (FRAC + 1);
-            const long long P0 = d[4] << (FRAC + 1), P1 = d[5] << (FRAC + 1);
             bool hv = false;
             i128 bestE = 0;
             int bestB = 0;
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-              if (k >= nb) break;
-              const int B = cb[k];
-              // Eq. 1 difference of relabelling the block A -> B under the frozen means (x 2^-16
-              // of the oracle's weighted dE): X = colour part + E_b part (int64, exact),
-              // dP = position part; E = X * 2^16 + lambda_pos * dP (128-bit)
-              const long long cB0 = (unsigned)rn[k].z & 0xffffu, cB1 = (unsigned)rn[k].z >> 16;
-              const long long cB2 = (unsigned)rn[k].w & 0xffffu;
-              const long long dB2 = 2 * (wA - wsum(cm[k]));
-              const long long X = (cB0 - cA0) * (n * (cB0 + cA0) - S0) + (cB1 - cA1) * (n * (cB1 + cA1) - S1) +
-                                  (cB2 - cA2) * (n * (cB2 + cA2) - S2) + a.lam_b * dB2;
-              const long long mB0 = rn[k].x, mB1 = rn[k].y;
-              const long long dP = (mB0 - mA0) * (n * (mB0 + mA0) - P0) + (mB1 - mA1) * (n * (mB1 + mA1) - P1);
-              const unsigned long long plo = (unsigned long long)a.lam_pos * (unsigned long long)dP;
-              const long long phi = __mul64hi(a.lam_pos, dP);
-              const i128 E = ((i128)X << 16) + (i128)(((unsigned __int128)(unsigned long long)phi << 64) | plo);
+            for (int k2 = 0; k2 < 4; k2++) {
+              if (k2 >= nb) break;
+              const int B = cb[k2];
+              const i128 E = energy<PIXEL>(recA, rn[k2], d, 2 * (wA - wsum(cm[k2])), a.lam_pos, a.lam_b);
               if (!hv || E < bestE || (E == bestE && B < bestB)) {
                 hv = true;
                 bestE = E;
@@ -714,9 +748,9 @@ __global__ void __launch_bounds__(K4B_THREADS, K4B_MIN_BLOCKS) k_sweep(const Pha
                 // passing the static gate (A passed it; others from their record flags)
                 ins = maskA;
 #pragma unroll
-                for (int k = 0; k < 4; k++)
-                  if (k < nb && cb[k] != Bm && (a.gating != 1 || (((unsigned)rn[k].w >> 16) & F_ACTIVE)))
-                    ins |= cm[k];
+                for (int k2 = 0; k2 < 4; k2++)
+                  if (k2 < nb && cb[k2] != Bm && (a.gating != 1 || (((unsigned)rn[k2].w >> 16) & F_ACTIVE)))
+                    ins |= cm[k2];
               }
             }
           }
@@ -871,9 +905,15 @@ void launch_eval(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
   else k_eval<false, false><<<grid, K4B_THREADS, 0, s>>>(a);
 }
 
+static int g_sweep_minb = 3;  // RAPID_SWEEP_MINB (2..4): CTAs per SM the register budget targets
+
 int sweep_occupancy() {
+  const char *e = getenv("RAPID_SWEEP_MINB");
+  if (e && e[0] >= '2' && e[0] <= '4') g_sweep_minb = e[0] - '0';
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sweep<true, true>, K4B_THREADS, 0);
+  if (g_sweep_minb == 2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sweep<true, true, 2>, K4B_THREADS, 0);
+  else if (g_sweep_minb == 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sweep<true, true, 4>, K4B_THREADS, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sweep<true, true, 3>, K4B_THREADS, 0);
   return nb < 1 ? 1 : nb;
 }
 
@@ -883,10 +923,15 @@ void launch_bset_build(const PhaseArgs &a, int grid, cudaStream_t s) {
 
 void launch_sweep(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
   const bool gated = a.size_mode != 0;
-  if (pixel && gated) k_sweep<true, true><<<grid, K4B_THREADS, 0, s>>>(a);
-  else if (pixel) k_sweep<true, false><<<grid, K4B_THREADS, 0, s>>>(a);
-  else if (gated) k_sweep<false, true><<<grid, K4B_THREADS, 0, s>>>(a);
-  else k_sweep<false, false><<<grid, K4B_THREADS, 0, s>>>(a);
+#define RAPID_SWEEP_LAUNCH(MB)                                                    \
+  if (pixel && gated) k_sweep<true, true, MB><<<grid, K4B_THREADS, 0, s>>>(a);    \
+  else if (pixel) k_sweep<true, false, MB><<<grid, K4B_THREADS, 0, s>>>(a);       \
+  else if (gated) k_sweep<false, true, MB><<<grid, K4B_THREADS, 0, s>>>(a);       \
+  else k_sweep<false, false, MB><<<grid, K4B_THREADS, 0, s>>>(a);
+  if (g_sweep_minb == 2) { RAPID_SWEEP_LAUNCH(2) }
+  else if (g_sweep_minb == 4) { RAPID_SWEEP_LAUNCH(4) }
+  else { RAPID_SWEEP_LAUNCH(3) }
+#undef RAPID_SWEEP_LAUNCH
 }
 
 void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {

@@ -26,6 +26,7 @@ struct Ctl {  // per-segmentation device control block (zeroed at the start of e
   unsigned int nwork[MAXS];
   unsigned int err;
   unsigned int vtotal, deg_total, npairs, atotal;
+  unsigned int mflag[2];  // cooperative merge match: pending flags per round parity
 };
 
 struct StagePlan {
@@ -674,6 +675,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       ma.candE = c->candE;
       ma.pairs = c->pairs;
       ma.npairs = &ctl->npairs;
+      ma.flag = ctl->mflag;
+      ma.bset = c->use_bset ? (const uint32_t *)c->bset.p : nullptr;
       ma.stage_info = &ctl->stage_info[st][0];
       launch_merge_round(ma, grid_k, s, &c->launches);
     }

@@ -12,7 +12,12 @@
 //   K9 final                    final grain upsample / pending remap (Table 1 grain)
 #include <cstdio>
 
+#include <algorithm>
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace rapid {
 
@@ -321,6 +326,7 @@ __device__ void hash_add(const MergeArgs &a, int V, int T, unsigned e) {
 // victims: head[V] = -1
 __global__ void k_merge_heads(const MergeArgs a) {
   if (*a.victim_any == 0u) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.npairs = 0u;  // this round's pair counter
   const unsigned nv = *a.total;
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += gridDim.x * blockDim.x)
     a.head[a.vlist[i]] = -1;
@@ -331,32 +337,47 @@ __global__ void k_merge_heads(const MergeArgs a) {
 // to len[V][L_q] — the same totals as summing over unordered adjacent pairs.  At gated
 // stages only worklist tiles can hold victim blocks (victims are active superpixels, and
 // active superpixels' blocks never leave the worklist tiles), so only those are scanned.
-__global__ void k_merge_adjacency(const MergeArgs a) {
+// One CTA per sweep tile; thread (r, q) owns blocks gx0+4q .. +3 of row gy0+r.  With boundary
+// sets (a.bset), only blocks whose bit is set are examined: a victim is an active superpixel
+// (it passed the static gate) and the sets hold every gated boundary block (sweep.cu).
+__global__ void __launch_bounds__(256) k_merge_adjacency(const MergeArgs a) {
   if (*a.victim_any == 0u) return;
   const StageDev &st = a.st;
+  const int nbx = st.nbx, nby = st.nby;
   const unsigned ntiles = a.worklist ? *a.nwork : (unsigned)(st.tiles_x * st.tiles_y) * (unsigned)a.B;
-  const size_t n = (size_t)ntiles * (TX * TY);
-  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
-       t += (size_t)gridDim.x * blockDim.x) {
-    const unsigned w = (unsigned)(t / (TX * TY));
-    const int off = (int)(t - (size_t)w * (TX * TY));
+  const int r = threadIdx.x >> 4, q = threadIdx.x & 15;
+  for (unsigned w = blockIdx.x; w < ntiles; w += gridDim.x) {
     const uint32_t tile = a.worklist ? (uint32_t)a.worklist[w] : w;
-    const uint32_t r = fdiv(tile, st.fd_tx), img = fdiv(r, st.fd_ty);
-    const int gx = (int)(tile - r * (uint32_t)st.tiles_x) * TX + (off % TX);
-    const int gy = (int)(r - img * (uint32_t)st.tiles_y) * TY + (off / TX);
-    if (gx >= st.nbx || gy >= st.nby) continue;
-    const int32_t *map = st.map + (size_t)img * st.nby * st.nbx;
-    const size_t p = (size_t)gy * st.nbx + gx;
-    const int la = map[p];
-    const int nq[4] = {gy > 0 ? map[p - st.nbx] : la, gx + 1 < st.nbx ? map[p + 1] : la,
-                       gy + 1 < st.nby ? map[p + st.nbx] : la, gx > 0 ? map[p - 1] : la};
-    if (nq[0] == la && nq[1] == la && nq[2] == la && nq[3] == la) continue;
+    const uint32_t rr = fdiv(tile, st.fd_tx), img = fdiv(rr, st.fd_ty);
+    const int gx0 = (int)(tile - rr * (uint32_t)st.tiles_x) * TX, gy0 = (int)(rr - img * (uint32_t)st.tiles_y) * TY;
+    const int gy = gy0 + r;
+    if (gy >= nby) continue;
+    unsigned m4 = 0xfu;  // blocks of this thread to examine
+    if (a.bset) {
+      const uint32_t *tw = a.bset + (size_t)tile * 32 + (r >> 1);
+      const uint32_t w0 = tw[(0 + 2 * (r & 1)) * (TY / 2)], w1 = tw[(1 + 2 * (r & 1)) * (TY / 2)];
+      m4 = ((w0 >> (2 * q)) & 1u) | (((w1 >> (2 * q)) & 1u) << 1) | (((w0 >> (2 * q + 1)) & 1u) << 2) |
+           (((w1 >> (2 * q + 1)) & 1u) << 3);
+    }
+    if (!m4) continue;
+    const int32_t *map = st.map + (size_t)img * nby * nbx;
     const int kb = (int)img * a.M;
-    if (!a.sp.victim[kb + la]) continue;
-    const unsigned ew = (unsigned)(st.xs[gx + 1] - st.xs[gx]), eh = (unsigned)(st.ys[gy + 1] - st.ys[gy]);
+    const unsigned eh = (unsigned)(st.ys[gy + 1] - st.ys[gy]);
 #pragma unroll
-    for (int q = 0; q < 4; q++)
-      if (nq[q] != la) hash_add(a, kb + la, kb + nq[q], (q & 1) ? eh : ew);
+    for (int k = 0; k < 4; k++) {
+      const int gx = gx0 + 4 * q + k;
+      if (!((m4 >> k) & 1u) || gx >= nbx) continue;
+      const size_t p = (size_t)gy * nbx + gx;
+      const int la = map[p];
+      const int nq[4] = {gy > 0 ? map[p - nbx] : la, gx + 1 < nbx ? map[p + 1] : la,
+                         gy + 1 < nby ? map[p + nbx] : la, gx > 0 ? map[p - 1] : la};
+      if (nq[0] == la && nq[1] == la && nq[2] == la && nq[3] == la) continue;
+      if (!a.sp.victim[kb + la]) continue;
+      const unsigned ew = (unsigned)(st.xs[gx + 1] - st.xs[gx]);
+#pragma unroll
+      for (int d = 0; d < 4; d++)
+        if (nq[d] != la) hash_add(a, kb + la, kb + nq[d], (d & 1) ? eh : ew);
+    }
   }
 }
 
@@ -472,18 +493,16 @@ __global__ void k_merge_fill(const MergeArgs a) {
 // reservations is the earliest pending edge at both ends, so the sequential order would
 // take it too.  Rounds repeat until no edge is pending; the result is order-independent.
 // mlock[] (per superpixel) and res[] (reservations) are zero / ~0 outside this kernel.
-__global__ void __launch_bounds__(1024) k_merge_match(const MergeArgs a) {
+// Cooperative (grid-synchronised) version: every round is three grid-wide passes over the
+// edges; a.flag[2] = "some edge still pending" per round parity, a.npairs the pair counter.
+__global__ void __launch_bounds__(256) k_merge_match(const MergeArgs a) {
   if (*a.victim_any == 0u) return;
-  __shared__ int s_any;
-  __shared__ unsigned s_np;
+  cg::grid_group grid = cg::this_grid();
   const unsigned ne = a.deg[*a.total];
-  if (threadIdx.x == 0) s_np = 0;
-  while (true) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_any = 0;
-    __syncthreads();
+  const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  for (unsigned round = 0;; round++) {
     int any = 0;
-    for (unsigned p = threadIdx.x; p < ne; p += blockDim.x) {
+    for (unsigned p = tid; p < ne; p += nth) {
       const int T = a.candT[p];
       if (T < 0) continue;
       const int V = a.candV[p];
@@ -495,36 +514,39 @@ __global__ void __launch_bounds__(1024) k_merge_match(const MergeArgs a) {
       atomicMin(&a.res[T], p);
       any = 1;
     }
-    if (any) s_any = 1;
-    __syncthreads();
-    if (!s_any) break;
-    for (unsigned p = threadIdx.x; p < ne; p += blockDim.x) {
+    if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(&a.flag[round & 1], 1u);
+    grid.sync();
+    const bool more = *reinterpret_cast<volatile unsigned *>(&a.flag[round & 1]) != 0u;
+    if (!more) break;
+    if (tid == 0) a.flag[(round + 1) & 1] = 0u;  // next round's flag (nobody sets it before the next sync)
+    for (unsigned p = tid; p < ne; p += nth) {
       const int T = a.candT[p];
       if (T < 0) continue;
       const int V = a.candV[p];
       if (a.res[V] == p && a.res[T] == p) {
         a.mlock[V] = 1u;
         a.mlock[T] = 1u;
-        a.res[T] = 0xffffffffu;  // V's reservation is released below
-        const unsigned q = atomicAdd(&s_np, 1u);
-        a.pairs[2 * q] = V;
-        a.pairs[2 * q + 1] = T;
+        const unsigned qq = atomicAdd(a.npairs, 1u);
+        a.pairs[2 * qq] = V;
+        a.pairs[2 * qq + 1] = T;
         a.candT[p] = -1;
       }
     }
-    __syncthreads();
-    for (unsigned p = threadIdx.x; p < ne; p += blockDim.x) {  // release reservations
+    grid.sync();
+    for (unsigned p = tid; p < ne; p += nth) {  // release reservations
       const int T = a.candT[p];
       const int V = a.candV[p];
       a.res[V] = 0xffffffffu;
       if (T >= 0) a.res[T] = 0xffffffffu;
     }
+    grid.sync();
   }
-  if (threadIdx.x == 0) {
-    *a.npairs = s_np;
+  if (tid == 0) {
+    const unsigned np = *a.npairs;
     a.stage_info[0] += *a.total;
-    a.stage_info[1] += s_np;
-    if (s_np) *a.remap_pending = 1u;
+    a.stage_info[1] += np;
+    if (np) *a.remap_pending = 1u;
+    a.flag[0] = a.flag[1] = 0u;
   }
 }
 
@@ -829,11 +851,24 @@ void launch_merge_round(const MergeArgs &a, int grid, cudaStream_t s, int *nlaun
   k_flag_scatter<<<nchunks, 256, 0, s>>>(a.sp.victim, a.K, a.chunk, a.vlist, a.victim_any);
   k_merge_heads<<<grid, 256, 0, s>>>(a);
   const size_t nb = (size_t)a.st.nbx * a.st.nby * a.B;
-  k_merge_adjacency<<<grid_for(nb, 256, 148 * 32), 256, 0, s>>>(a);
+  (void)nb;
+  k_merge_adjacency<<<148 * 8, 256, 0, s>>>(a);
   k_merge_degree<<<grid, 256, 0, s>>>(a);
   k_merge_scan_deg<<<1, 1024, 0, s>>>(a);
   k_merge_fill<<<grid, 256, 0, s>>>(a);
-  k_merge_match<<<1, 1024, 0, s>>>(a);
+  {
+    static int coop_grid = 0;
+    if (!coop_grid) {
+      int nbk = 0, dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbk, k_merge_match, 256, 0);
+      coop_grid = sms * std::max(1, std::min(nbk, 4));
+    }
+    MergeArgs aa = a;
+    void *args[] = {&aa};
+    cudaLaunchCooperativeKernel((const void *)k_merge_match, coop_grid, 256, args, 0, s);
+  }
   k_merge_apply<<<grid, 256, 0, s>>>(a);
   k_merge_cleanup<<<grid, 256, 0, s>>>(a);
   k_merge_done<<<1, 1, 0, s>>>(a);

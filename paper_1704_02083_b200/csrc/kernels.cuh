@@ -66,6 +66,8 @@ struct MergeArgs {
   int32_t *pairs;            // merges (A, T)
   unsigned int *npairs;
   unsigned long long *stage_info; // [4]: victims, merges, active tiles, -
+  unsigned int *flag;        // [2] cooperative match: pending-edge flags (zero outside)
+  const uint32_t *bset;      // boundary sets of the stage (null: scan every block)
 };
 
 struct PredictArgs {

@@ -96,7 +96,7 @@ struct rapid_ctx {
   // host-API staging
   DevBuf himg, hlab;
   // occupancy
-  int scan_grid = 0, eval_grid = 0, sweep_grid = 0;  // persistent grid sizes (CTAs)
+  int scan_grid = 0, eval_grid = 0, sweep_grid = 0, tiles_grid = 0;  // persistent grid sizes (CTAs)
   bool use_bset = true;  // RAPID_SWEEP=scan selects the full-scan path K4a + K4b (A/B testing)
   // CUDA graph of the whole segmentation (one launch per call): captured on a private stream,
   // replayed while the key (buffers, geometry, params, profiling level, plan) is unchanged
@@ -557,7 +557,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       ba.worklist = use_work ? (const int32_t *)c->work.p : nullptr;
       ba.nwork = &ctl->nwork[st];
       ba.bset = (uint32_t *)c->bset.p;
-      launch_bset_build(ba, c->sm_count * 8, s);
+      launch_bset_build(ba, has_tmap[st] ? tmaps[st].b : nullptr, has_tmap[st] ? c->tiles_grid : c->sm_count * 8, s);
       c->launches++;
     }
     if (c->prof >= 2 && use_work) {  // profiling only: algorithmic window of the gated stage
@@ -678,7 +678,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       ma.flag = ctl->mflag;
       ma.bset = c->use_bset ? (const uint32_t *)c->bset.p : nullptr;
       ma.stage_info = &ctl->stage_info[st][0];
-      launch_merge_round(ma, grid_k, s, &c->launches);
+      launch_merge_round(ma, has_tmap[st] ? tmaps[st].b : nullptr, c->tiles_grid, grid_k, s, &c->launches);
     }
     if (stop_at(RAPID_STOP_AFTER_MERGE, st, 0, 0)) {
       remap_in_place(st);
@@ -813,6 +813,7 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   c->scan_grid = c->sm_count * scan_occupancy();
   c->eval_grid = c->sm_count * eval_occupancy();
   c->sweep_grid = c->sm_count * sweep_occupancy();
+  c->tiles_grid = c->sm_count * tiles_occupancy();
   {
     const char *e = getenv("RAPID_SWEEP");
     c->use_bset = !(e && strcmp(e, "scan") == 0);

@@ -285,44 +285,6 @@ __global__ void k_flag_scatter(const uint8_t *__restrict__ flags, int n, const u
 }
 
 // ------------------------------------------------------------------ K6: merge round
-__device__ __forceinline__ unsigned long long hmix(unsigned long long k) {
-  k ^= k >> 33;
-  k *= 0xff51afd7ed558ccdull;
-  k ^= k >> 33;
-  k *= 0xc4ceb9fe1a85ec53ull;
-  k ^= k >> 33;
-  return k;
-}
-constexpr unsigned long long HEMPTY = ~0ull;
-
-__device__ void hash_add(const MergeArgs &a, int V, int T, unsigned e) {
-  const unsigned long long key = ((unsigned long long)(unsigned)V << 32) | (unsigned)T;
-  unsigned long long h = hmix(key) & a.hmask;
-  while (true) {
-    // most calls find an existing key: a plain (volatile) read avoids contended CAS
-    const unsigned long long seen = *reinterpret_cast<volatile unsigned long long *>(&a.hkeys[h]);
-    if (seen == key) {
-      atomicAdd(&a.hvals[h], e);
-      return;
-    }
-    if (seen != HEMPTY) {
-      h = (h + 1) & a.hmask;
-      continue;
-    }
-    const unsigned long long old = atomicCAS(&a.hkeys[h], HEMPTY, key);
-    if (old == HEMPTY) {
-      atomicAdd(&a.hvals[h], e);
-      a.hnext[h] = atomicExch(&a.head[V], (int)h);
-      return;
-    }
-    if (old == key) {
-      atomicAdd(&a.hvals[h], e);
-      return;
-    }
-    h = (h + 1) & a.hmask;
-  }
-}
-
 // victims: head[V] = -1
 __global__ void k_merge_heads(const MergeArgs a) {
   if (*a.victim_any == 0u) return;
@@ -844,7 +806,8 @@ void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s) {
   k_snapshot<<<g, 256, 0, s>>>(a);
 }
 
-void launch_merge_round(const MergeArgs &a, int grid, cudaStream_t s, int *nlaunch) {
+void launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int grid, cudaStream_t s,
+                        int *nlaunch) {
   const int nchunks = (a.K + CHUNK - 1) / CHUNK;
   k_flag_count<<<nchunks, 256, 0, s>>>(a.sp.victim, a.K, a.chunk, a.victim_any);
   k_scan_chunks<<<1, 1024, 0, s>>>(a.chunk, nchunks, a.total, a.victim_any);
@@ -852,7 +815,7 @@ void launch_merge_round(const MergeArgs &a, int grid, cudaStream_t s, int *nlaun
   k_merge_heads<<<grid, 256, 0, s>>>(a);
   const size_t nb = (size_t)a.st.nbx * a.st.nby * a.B;
   (void)nb;
-  k_merge_adjacency<<<148 * 8, 256, 0, s>>>(a);
+  if (!launch_merge_adjacency_tma(a, tmap, tgrid, s)) k_merge_adjacency<<<148 * 8, 256, 0, s>>>(a);
   k_merge_degree<<<grid, 256, 0, s>>>(a);
   k_merge_scan_deg<<<1, 1024, 0, s>>>(a);
   k_merge_fill<<<grid, 256, 0, s>>>(a);

@@ -70,6 +70,45 @@ struct MergeArgs {
   const uint32_t *bset;      // boundary sets of the stage (null: scan every block)
 };
 
+// ---- merge adjacency hash (open addressing, (victim, neighbour) -> shared edge length)
+__device__ __forceinline__ unsigned long long hmix(unsigned long long k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
+constexpr unsigned long long HEMPTY = ~0ull;
+
+__device__ __forceinline__ void hash_add(const MergeArgs &a, int V, int T, unsigned e) {
+  const unsigned long long key = ((unsigned long long)(unsigned)V << 32) | (unsigned)T;
+  unsigned long long h = hmix(key) & a.hmask;
+  while (true) {
+    // most calls find an existing key: a plain (volatile) read avoids contended CAS
+    const unsigned long long seen = *reinterpret_cast<volatile unsigned long long *>(&a.hkeys[h]);
+    if (seen == key) {
+      atomicAdd(&a.hvals[h], e);
+      return;
+    }
+    if (seen != HEMPTY) {
+      h = (h + 1) & a.hmask;
+      continue;
+    }
+    const unsigned long long old = atomicCAS(&a.hkeys[h], HEMPTY, key);
+    if (old == HEMPTY) {
+      atomicAdd(&a.hvals[h], e);
+      a.hnext[h] = atomicExch(&a.head[V], (int)h);
+      return;
+    }
+    if (old == key) {
+      atomicAdd(&a.hvals[h], e);
+      return;
+    }
+    h = (h + 1) & a.hmask;
+  }
+}
+
 struct PredictArgs {
   StageDev st;
   SpDev sp;
@@ -137,7 +176,7 @@ void launch_scan(const PhaseArgs &a, const void *tmap, int grid, cudaStream_t s)
 void launch_eval(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
 void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
 // boundary-set sweep: K4 build (once per stage) and the fused bitset-driven sweep
-void launch_bset_build(const PhaseArgs &a, int grid, cudaStream_t s);
+void launch_bset_build(const PhaseArgs &a, const void *tmap, int grid, cudaStream_t s);
 void launch_sweep(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
 int sweep_occupancy();
 int scan_occupancy();
@@ -146,7 +185,10 @@ constexpr int CAND_SLACK_PER_WARP = 64;  // chunked reservations: unused tail pe
 // encode a 3-D TMA descriptor {nbx, nby, B} of int32 with box {TX+4, TY+2, 1};
 // false when nbx*4 is not a multiple of 16 B (the LDG loader is used then)
 bool make_label_tmap(void *tmap64B, int32_t *base, int nbx, int nby, int B);
-void launch_merge_round(const MergeArgs &a, int grid, cudaStream_t s, int *nlaunch);
+void launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int grid, cudaStream_t s,
+                        int *nlaunch);
+bool launch_merge_adjacency_tma(const MergeArgs &a, const void *tmap, int grid, cudaStream_t s);
+int tiles_occupancy();
 void launch_predict(const PredictArgs &a, int grid, cudaStream_t s, int *nlaunch);
 void launch_transition(const TransArgs &a, cudaStream_t s);
 void launch_recount(const RecountArgs &a, bool pixel, int grid, cudaStream_t s, int *nlaunch);

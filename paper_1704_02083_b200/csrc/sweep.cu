@@ -521,6 +521,148 @@ __global__ void __launch_bounds__(256) k_bset_build(const PhaseArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ TMA tile streamer
+// Persistent warp-specialised CTAs over the sweep tiles (worklist or all): one producer lane
+// streams (TY+2) x (TX+8) label boxes with TMA into an NSTAGE ring (full/empty mbarriers, as
+// K4a); 8 consumer warps each take two tile rows, every lane two adjacent columns (one block
+// of each column colour).  OP selects the per-stage pass:
+//   TILE_BSET  boundary-set build: bit = boundary (Eq. 2) and static gate; a lane's two
+//              columns have colours cx = 0, 1, so each row's two words are two ballots.
+//   TILE_ADJ   merge adjacency (O7 step 1): boundary blocks of victims add their shared edge
+//              lengths to the (victim, neighbour) hash.
+constexpr int TILE_BSET = 0, TILE_ADJ = 1;
+
+template <int OP>
+__global__ void __launch_bounds__(K4A_THREADS) k_tiles(const PhaseArgs a, const MergeArgs ma,
+                                                       const __grid_constant__ CUtensorMap tmap) {
+  __shared__ __align__(128) int32_t buf[NSTAGE][STAGE_INTS];
+  __shared__ __align__(8) uint64_t full[NSTAGE], empty[NSTAGE];
+  __shared__ int4 s_info[NSTAGE];  // gx0, gy0, img, border
+  if (OP == TILE_ADJ && *ma.victim_any == 0u) return;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const StageDev &st = a.st;
+  const int nbx = st.nbx, nby = st.nby;
+  const int tiles_x = st.tiles_x, tiles_y = st.tiles_y;
+  const unsigned ntiles = a.worklist ? *a.nwork : (unsigned)(tiles_x * tiles_y) * (unsigned)a.B;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NSTAGE; i++) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NWARP);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == NWARP) {  // ---- producer
+    for (unsigned kb = 0; blockIdx.x + kb * gridDim.x < ntiles; kb += 32) {
+      const unsigned wl = blockIdx.x + (kb + lane) * gridDim.x;
+      int4 inf = make_int4(0, 0, 0, 0);
+      if (wl < ntiles) {
+        const uint32_t t = a.worklist ? (uint32_t)a.worklist[wl] : wl;
+        const uint32_t r = fdiv(t, st.fd_tx), img = fdiv(r, st.fd_ty);
+        const int gx0 = (int)(t - r * (uint32_t)tiles_x) * TX, gy0 = (int)(r - img * (uint32_t)tiles_y) * TY;
+        const int border = (gx0 == 0 || gy0 == 0 || gx0 + TX + 1 > nbx || gy0 + TY + 1 > nby) ? 1 : 0;
+        inf = make_int4(gx0, gy0, (int)img, border);
+      }
+      for (int j = 0; j < 32; j++) {
+        const unsigned k = kb + j;
+        if (blockIdx.x + k * gridDim.x >= ntiles) break;  // warp-uniform
+        int4 v;
+        v.x = __shfl_sync(FULL, inf.x, j);
+        v.y = __shfl_sync(FULL, inf.y, j);
+        v.z = __shfl_sync(FULL, inf.z, j);
+        v.w = __shfl_sync(FULL, inf.w, j);
+        if (lane == 0) {
+          const int si = (int)(k % NSTAGE);
+          if (k >= NSTAGE) mbar_wait(&empty[si], ((k / NSTAGE) - 1) & 1u);
+          s_info[si] = v;
+          fence_proxy_async();
+          mbar_expect_tx(&full[si], TILE_BYTES);
+          tma_load_3d(&buf[si][0], &tmap, v.x - HX, v.y - 1, v.z, &full[si]);
+        }
+        __syncwarp();
+      }
+    }
+    return;
+  }
+  // ---- consumers: rows 2*warp, 2*warp+1 of the tile; columns 2*lane, 2*lane+1
+  int last = -1;
+  bool last_flag = false;
+  for (unsigned k = 0;; k++) {
+    const unsigned w = blockIdx.x + k * gridDim.x;
+    if (w >= ntiles) break;
+    const int si = (int)(k % NSTAGE);
+    mbar_wait(&full[si], (k / NSTAGE) & 1u);
+    const int4 inf = s_info[si];
+    const int gx0 = inf.x, gy0 = inf.y, img = inf.z;
+    int32_t *box = buf[si];
+    if (inf.w) {  // TMA zero-fills outside the image; 0 is a label: mark "no block" (-1)
+      for (int idx = lane; idx < 4 * BOXW; idx += 32) {
+        const int r = idx / BOXW, cc = idx - r * BOXW;
+        const int y = gy0 + 2 * warp - 1 + r, x = gx0 + cc - HX;
+        if (x < 0 || x >= nbx || y < 0 || y >= nby) box[(2 * warp + r) * BOXW + cc] = -1;
+      }
+      __syncwarp();
+    }
+    const int kb = img * a.M;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int rr = 2 * warp + h;  // tile row
+      const int32_t *up = box + rr * BOXW + HX, *mid = up + BOXW, *dn = mid + BOXW;
+      const int2 U = *reinterpret_cast<const int2 *>(up + 2 * lane);
+      const int2 Mv = *reinterpret_cast<const int2 *>(mid + 2 * lane);
+      const int2 D = *reinterpret_cast<const int2 *>(dn + 2 * lane);
+      const int Wn = mid[2 * lane - 1], En = mid[2 * lane + 2];
+      const int L[2] = {Mv.x, Mv.y}, N[2] = {U.x, U.y}, S[2] = {D.x, D.y}, Wv[2] = {Wn, Mv.x}, Ev[2] = {Mv.y, En};
+      bool bnd[2];
+#pragma unroll
+      for (int c = 0; c < 2; c++)
+        bnd[c] = L[c] >= 0 && ((N[c] >= 0 && N[c] != L[c]) | (S[c] >= 0 && S[c] != L[c]) |
+                               (Wv[c] >= 0 && Wv[c] != L[c]) | (Ev[c] >= 0 && Ev[c] != L[c]));
+      if (OP == TILE_BSET) {
+        bool bit[2];
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+          bit[c] = bnd[c];
+          if (bnd[c] && a.gating == 1) {
+            if (kb + L[c] != last) {  // cache keyed by the global id (images share local ids)
+              last = kb + L[c];
+              last_flag = a.sp.active[kb + L[c]] != 0;
+            }
+            bit[c] = last_flag;
+          }
+        }
+        const unsigned w0 = __ballot_sync(FULL, bit[0]), w1 = __ballot_sync(FULL, bit[1]);
+        if (lane == 0) {
+          const uint32_t tile = ((uint32_t)img * (uint32_t)tiles_y + (uint32_t)(gy0 / TY)) * (uint32_t)tiles_x +
+                                (uint32_t)(gx0 / TX);
+          uint32_t *tw = a.bset + (size_t)tile * BSET_WORDS_PER_TILE + (rr >> 1);
+          tw[(0 + 2 * (rr & 1)) * (TY / 2)] = w0;
+          tw[(1 + 2 * (rr & 1)) * (TY / 2)] = w1;
+        }
+      } else {  // TILE_ADJ
+        const int gy = gy0 + rr;
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+          if (!bnd[c]) continue;
+          if (kb + L[c] != last) {
+            last = kb + L[c];
+            last_flag = ma.sp.victim[kb + L[c]] != 0;
+          }
+          if (!last_flag) continue;
+          const int gx = gx0 + 2 * lane + c;
+          const unsigned ew = (unsigned)(st.xs[gx + 1] - st.xs[gx]), eh = (unsigned)(st.ys[gy + 1] - st.ys[gy]);
+          const int nq[4] = {N[c], Ev[c], S[c], Wv[c]};
+#pragma unroll
+          for (int d = 0; d < 4; d++)
+            if (nq[d] >= 0 && nq[d] != L[c]) hash_add(ma, kb + L[c], kb + nq[d], (d & 1) ? eh : ew);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[si]);
+  }
+}
+
 // lam * v exactly, for 0 <= lam < 2^31 and any int64 v: two 32 x 32 -> 64 products
 __device__ __forceinline__ i128 mul_u31_s64(long long lam, long long v) {
   const unsigned long long p0 = (unsigned long long)(uint32_t)lam * (uint32_t)v;  // IMAD.WIDE.U32
@@ -917,8 +1059,32 @@ int sweep_occupancy() {
   return nb < 1 ? 1 : nb;
 }
 
-void launch_bset_build(const PhaseArgs &a, int grid, cudaStream_t s) {
-  k_bset_build<<<grid, 256, 0, s>>>(a);
+void launch_bset_build(const PhaseArgs &a, const void *tmap, int grid, cudaStream_t s) {
+  if (tmap) {
+    MergeArgs none{};
+    k_tiles<TILE_BSET><<<grid, K4A_THREADS, 0, s>>>(a, none, *(const CUtensorMap *)tmap);
+  } else {
+    k_bset_build<<<grid, 256, 0, s>>>(a);
+  }
+}
+
+int tiles_occupancy() {
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tiles<TILE_ADJ>, K4A_THREADS, 0);
+  return nb < 1 ? 1 : nb;
+}
+
+bool launch_merge_adjacency_tma(const MergeArgs &m, const void *tmap, int grid, cudaStream_t s) {
+  if (!tmap) return false;
+  PhaseArgs a{};
+  a.st = m.st;
+  a.sp = m.sp;
+  a.B = m.B;
+  a.M = m.M;
+  a.worklist = m.worklist;
+  a.nwork = m.nwork;
+  k_tiles<TILE_ADJ><<<grid, K4A_THREADS, 0, s>>>(a, m, *(const CUtensorMap *)tmap);
+  return true;
 }
 
 void launch_sweep(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {

@@ -183,15 +183,51 @@ __device__ __forceinline__ void make_rec(const SpDev &sp, int k) {
 }
 
 __global__ void k_snapshot(const SnapArgs a) {
-  // full refresh (stamp 0) or only the superpixels stamped dirty by the previous phase; four
-  // stamps per thread (one 16-B load; the stamp array is padded to a multiple of 4)
+  // full refresh (stamp 0) or only the superpixels stamped dirty by the previous phase.  A warp
+  // takes 128 consecutive stamps (one 16-B load per lane; the array is padded to a multiple of
+  // 4), compacts the dirty ones and refreshes them 32 at a time (one record per lane).
+  const int lane = lane_id();
   const int n4 = (a.K + 3) >> 2;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
-    const uint4 s4 = a.stamp ? *reinterpret_cast<const uint4 *>(a.sp.dirty + 4 * (size_t)i) : make_uint4(0, 0, 0, 0);
-    const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
+  const int nchunks = (n4 + 31) >> 5;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int ch = wid; ch < nchunks; ch += nw) {
+    const int i = ch * 32 + lane;
+    unsigned m = 0;
+    if (i < n4) {
+      const uint4 s4 = a.stamp ? *reinterpret_cast<const uint4 *>(a.sp.dirty + 4 * (size_t)i) : make_uint4(0, 0, 0, 0);
+      const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
-    for (int j = 0; j < 4; j++)
-      if (4 * i + j < a.K && (a.stamp == 0u || sv[j] == a.stamp)) make_rec(a.sp, 4 * i + j);
+      for (int j = 0; j < 4; j++)
+        if (4 * i + j < a.K && (a.stamp == 0u || sv[j] == a.stamp)) m |= 1u << j;
+    }
+    unsigned incl = __popc(m);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const unsigned total = __shfl_sync(FULL, incl, 31);
+    for (unsigned rb = 0; rb < total; rb += 32) {
+      const unsigned k = rb + lane;
+      int j = 0;  // source lane: #lanes with incl <= k
+#pragma unroll
+      for (int h = 16; h > 0; h >>= 1) {
+        const unsigned v = __shfl_sync(FULL, incl, j + h - 1);
+        if (v <= k) j += h;
+      }
+      const unsigned mj = __shfl_sync(FULL, m, j);
+      unsigned r = k - (__shfl_sync(FULL, incl, j) - __popc(mj));
+      if (k < total) {
+        int bit = 0;  // r-th set bit of the 4-bit mask
+        unsigned mm = mj;
+        while (r) {
+          mm &= mm - 1;
+          r--;
+        }
+        bit = __ffs(mm) - 1;
+        make_rec(a.sp, 4 * (ch * 32 + j) + bit);
+      }
+    }
   }
 }
 
@@ -801,8 +837,8 @@ void launch_stats0(const InitArgs &a, cudaStream_t s) {
 }
 
 void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s) {
-  // one pass: every thread checks 4 stamps once (grid capped at `grid` x 2)
-  const int g = grid_for(((size_t)a.K + 3) / 4, 256, 2 * grid);
+  // one pass: every warp checks 128 stamps once (grid capped at `grid` x 2)
+  const int g = grid_for(((size_t)a.K + 127) / 128 * 32, 256, 2 * grid);
   k_snapshot<<<g, 256, 0, s>>>(a);
 }
 

@@ -101,6 +101,7 @@ struct rapid_ctx {
   // CUDA graph of the whole segmentation (one launch per call): captured on a private stream,
   // replayed while the key (buffers, geometry, params, profiling level, plan) is unchanged
   bool use_graph = true;  // RAPID_NO_GRAPH=1 enqueues the kernels one by one (A/B testing)
+  bool l2_persist = false;  // RAPID_L2_PERSIST=1: L2 access-policy window on the sums (graph path)
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t gexec = nullptr;
   unsigned plan_gen = 0;
@@ -825,6 +826,8 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   {
     const char *e = getenv("RAPID_NO_GRAPH");
     c->use_graph = !(e && e[0] == '1');
+    e = getenv("RAPID_L2_PERSIST");
+    c->l2_persist = e && e[0] == '1';
   }
   rc = cuda_check(c, cudaDeviceSynchronize(), "rapid_init");
   if (rc) {
@@ -862,9 +865,30 @@ int rapid_segment(rapid_ctx *c, const uint8_t *image, int32_t H, int32_t W, cons
         cudaGraphExecDestroy(c->gexec);
         c->gexec = nullptr;
       }
-      if (!c->cap_stream && (rc = cuda_check(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking),
-                                             "capture stream")))
-        return rc;
+      if (!c->cap_stream) {
+        if ((rc = cuda_check(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking), "capture stream")))
+          return rc;
+        if (c->l2_persist) {  // keep the per-superpixel sums (atomic targets) resident in L2
+          int max_persist = 0, max_win = 0;
+          cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, c->device);
+          cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
+          const size_t bytes = std::min<size_t>((size_t)c->cap_sp * SUMW * 8, (size_t)max_win);
+          if (max_persist > 0 && bytes > 0) {
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(bytes, (size_t)max_persist));
+            cudaStreamAttrValue v{};
+            v.accessPolicyWindow.base_ptr = c->sums;
+            v.accessPolicyWindow.num_bytes = bytes;
+            v.accessPolicyWindow.hitRatio = std::min(1.0f, (float)max_persist / (float)bytes);
+            v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            cudaStreamSetAttribute(c->cap_stream, cudaStreamAttributeAccessPolicyWindow, &v);
+            if (getenv("RAPID_VERBOSE"))
+              fprintf(stderr, "rapid: L2 persisting window %zu B (max persist %d, max window %d)\n", bytes,
+                      max_persist, max_win);
+          }
+          cudaGetLastError();
+        }
+      }
       if ((rc = cuda_check(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal),
                            "begin capture")))
         return rc;

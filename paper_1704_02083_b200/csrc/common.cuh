@@ -147,6 +147,14 @@ __device__ __forceinline__ WarpRun warp_runs(bool valid, int key) {
   return r;
 }
 
+// int64 atomic add that asks L2 to keep the line (evict_last): the per-superpixel sums are
+// the atomic targets of every phase and must not be displaced by the streaming label reads
+__device__ __forceinline__ void red_add_keep(unsigned long long *p, unsigned long long v) {
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+
 __device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[6], bool negate,
                                          unsigned long long *sums, uint32_t *dirty, uint32_t stamp) {
   if (__ballot_sync(FULL, valid) == 0u) return;  // warp-uniform
@@ -170,7 +178,7 @@ __device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[
     const long long tot[6] = {(long long)v0, (long long)v1, (long long)v2, (long long)v3, v4, v5};
     unsigned long long *s = sums + (size_t)key * SUMW;
 #pragma unroll
-    for (int f = 0; f < 6; f++) atomicAdd(&s[f], (unsigned long long)(negate ? -tot[f] : tot[f]));
+    for (int f = 0; f < 6; f++) red_add_keep(&s[f], (unsigned long long)(negate ? -tot[f] : tot[f]));
     if (dirty != nullptr) dirty[key] = stamp;
   }
 }

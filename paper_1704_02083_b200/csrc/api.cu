@@ -615,7 +615,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           if (gated_sz) cudaMemsetAsync(c->out, 0, sizeof(int32_t) * K, s);
           if (c->use_bset) {
             Timer t2(c, s, RAPID_K_PROPOSE, st);
-            launch_sweep(pa, pixel, c->sweep_grid, s);
+            launch_sweep(pa, pixel, c->sm_count, s);
             c->launches++;
           } else {
             {

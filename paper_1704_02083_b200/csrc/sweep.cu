@@ -675,26 +675,27 @@ __device__ __forceinline__ i128 mul_u31_s64(long long lam, long long v) {
 // and dP the position part (exact in int64).  At the pixel stage (n = 1, values
 // < 2^8, coordinates < 2^16) every factor fits 32 bits, so each product is one IMAD.WIDE.
 template <bool PIXEL>
-__device__ __forceinline__ i128 energy(const Rec &ra, const int4 rb, const long long d[6], long long dB2,
+__device__ __forceinline__ i128 energy(const Rec &ra, const int4 rb, const int d[6], long long dB2,
                                        long long lam_pos, long long lam_b) {
   const int cA0 = (int)(ra.cq01 & 0xffffu), cA1 = (int)(ra.cq01 >> 16), cA2 = (int)(ra.cq2f & 0xffffu);
   const int cB0 = (int)((unsigned)rb.z & 0xffffu), cB1 = (int)((unsigned)rb.z >> 16);
   const int cB2 = (int)((unsigned)rb.w & 0xffffu);
   long long X, dP;
   if (PIXEL) {
-    X = (long long)(cB0 - cA0) * (int)(cB0 + cA0 - ((int)d[1] << (FRAC + 1))) +
-        (long long)(cB1 - cA1) * (int)(cB1 + cA1 - ((int)d[2] << (FRAC + 1))) +
-        (long long)(cB2 - cA2) * (int)(cB2 + cA2 - ((int)d[3] << (FRAC + 1))) +
-        (long long)(int)lam_b * (int)dB2;
-    dP = (long long)(rb.x - ra.mux) * (int)(rb.x + ra.mux - ((int)d[4] << (FRAC + 1))) +
-         (long long)(rb.y - ra.muy) * (int)(rb.y + ra.muy - ((int)d[5] << (FRAC + 1)));
+    X = (long long)(cB0 - cA0) * (cB0 + cA0 - (d[1] << (FRAC + 1))) +
+        (long long)(cB1 - cA1) * (cB1 + cA1 - (d[2] << (FRAC + 1))) +
+        (long long)(cB2 - cA2) * (cB2 + cA2 - (d[3] << (FRAC + 1))) + (long long)(int)lam_b * (int)dB2;
+    dP = (long long)(rb.x - ra.mux) * (rb.x + ra.mux - (d[4] << (FRAC + 1))) +
+         (long long)(rb.y - ra.muy) * (rb.y + ra.muy - (d[5] << (FRAC + 1)));
   } else {
-    const long long n = d[0];
+    // n <= 4096 and sums < 2^21 (b <= 64): the colour factors fit 32 bits, the position
+    // factors need 64 (n * (mB + mA) < 2^37)
+    const int n = d[0];
     X = (long long)(cB0 - cA0) * (n * (cB0 + cA0) - (d[1] << (FRAC + 1))) +
         (long long)(cB1 - cA1) * (n * (cB1 + cA1) - (d[2] << (FRAC + 1))) +
         (long long)(cB2 - cA2) * (n * (cB2 + cA2) - (d[3] << (FRAC + 1))) + lam_b * dB2;
-    dP = (long long)(rb.x - ra.mux) * (n * ((long long)rb.x + ra.mux) - (d[4] << (FRAC + 1))) +
-         (long long)(rb.y - ra.muy) * (n * ((long long)rb.y + ra.muy) - (d[5] << (FRAC + 1)));
+    dP = (long long)(rb.x - ra.mux) * ((long long)n * ((long long)rb.x + ra.mux) - ((long long)d[4] << (FRAC + 1))) +
+         (long long)(rb.y - ra.muy) * ((long long)n * ((long long)rb.y + ra.muy) - ((long long)d[5] << (FRAC + 1)));
   }
   return ((i128)X << 16) + mul_u31_s64(lam_pos, dP);
 }
@@ -714,7 +715,9 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
   const unsigned ngroups = (ntiles * (TY / 2) + G - 1) / G;
   const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const int colour = a.cx | (a.cy << 1);
-  unsigned c_cand = 0, c_topo = 0, c_prop = 0, c_srej = 0, c_commit = 0;
+  __shared__ unsigned s_cnt[5];  // cand, topo, prop, srej, commit (per CTA; flushed at the end)
+  if (threadIdx.x < 5) s_cnt[threadIdx.x] = 0u;
+  __syncthreads();
   unsigned long long pbase = 0;  // this warp's reserved proposal slots
   int pleft = 0;
   for (unsigned g = gw; g < ngroups; g += nw) {
@@ -757,7 +760,7 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
       int A = 0, Bm = 0, kb = img * a.M, gx = 0, gy = 0;
       unsigned ins = 0;
       uint32_t rgb = 0;
-      long long d[6] = {0, 0, 0, 0, 0, 0};
+      int d[6] = {0, 0, 0, 0, 0, 0};  // block data: n, colour sums, position sums (all < 2^31)
       if (have) {
         const unsigned bit = nth_set_bit(wj, k - ej);
         gx = (int)(pj & 0xffffu) + 2 * (int)bit;
@@ -844,24 +847,24 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
           }
           emit = cand && topo_ok;
           if (emit) {
-            long long bw = 1, bh = 1;  // E_b edge weights: N/S edges have length bw, W/E bh
+            int bw = 1, bh = 1;  // E_b edge weights: N/S edges have length bw, W/E bh
             if (PIXEL) {
               d[0] = 1; d[1] = rgb & 0xffu; d[2] = (rgb >> 8) & 0xffu; d[3] = rgb >> 16; d[4] = gx; d[5] = gy;
             } else {
               bw = bx1 - bx0;
               bh = by1 - by0;
               d[0] = bw * bh;
-              d[1] = (long long)(pk & 0x1FFFFFull);
-              d[2] = (long long)((pk >> 21) & 0x1FFFFFull);
-              d[3] = (long long)(pk >> 42);
-              d[4] = bh * ((bw * (2 * (long long)bx0 + bw - 1)) / 2);
-              d[5] = bw * ((bh * (2 * (long long)by0 + bh - 1)) / 2);
+              d[1] = (int)(pk & 0x1FFFFFull);
+              d[2] = (int)((pk >> 21) & 0x1FFFFFull);
+              d[3] = (int)(pk >> 42);
+              d[4] = bh * ((bw * (2 * bx0 + bw - 1)) / 2);
+              d[5] = bw * ((bh * (2 * by0 + bh - 1)) / 2);
             }
             // weight of the slots in mask s: N (1), S (4) edges have length bw; E (2), W (8) bh
-            auto wsum = [&](unsigned msk) -> long long {
-              return PIXEL ? (long long)__popc(msk) : bw * __popc(msk & 5u) + bh * __popc(msk & 10u);
+            auto wsum = [&](unsigned msk) -> int {
+              return PIXEL ? __popc(msk) : bw * __popc(msk & 5u) + bh * __popc(msk & 10u);
             };
-            const long long wA = wsum(maskA);
+            const int wA = wsum(maskA);
             bool hv = false;
             i128 bestE = 0;
             int bestB = 0;
@@ -869,7 +872,7 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
             for (int k2 = 0; k2 < 4; k2++) {
               if (k2 >= nb) break;
               const int B = cb[k2];
-              const i128 E = energy<PIXEL>(recA, rn[k2], d, 2 * (wA - wsum(cm[k2])), a.lam_pos, a.lam_b);
+              const i128 E = energy<PIXEL>(recA, rn[k2], d, 2ll * (wA - wsum(cm[k2])), a.lam_pos, a.lam_b);
               if (!hv || E < bestE || (E == bestE && B < bestB)) {
                 hv = true;
                 bestE = E;
@@ -898,11 +901,17 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
           }
         }
       }
-      c_cand += __popc(__ballot_sync(FULL, cand));
-      c_topo += __popc(__ballot_sync(FULL, emit));
-      c_srej += __popc(__ballot_sync(FULL, srej));
+      {
+        const unsigned bc = __ballot_sync(FULL, cand), be = __ballot_sync(FULL, emit);
+        const unsigned bs = __ballot_sync(FULL, srej), bp = __ballot_sync(FULL, prop);
+        if (lane == 0) {
+          atomicAdd(&s_cnt[0], __popc(bc));
+          atomicAdd(&s_cnt[1], __popc(be));
+          if (bs) atomicAdd(&s_cnt[3], __popc(bs));
+          if (bp) atomicAdd(&s_cnt[2], __popc(bp));
+        }
+      }
       const unsigned pm = __ballot_sync(FULL, prop);
-      c_prop += __popc(pm);
       if (pm) {
         const size_t idx = ((size_t)img * nby + gy) * nbx + gx;
         if (!GATED) {  // size_mode NONE: no budget to check, commit in place
@@ -910,9 +919,10 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
             st.map[idx] = Bm;
             bset_insert(a.bset, st, img, gx, gy, ins);
           }
-          agg_sums(prop, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp);
-          agg_sums(prop, kb + Bm, d, false, a.sp.sums, a.sp.dirty, a.stamp);
-          c_commit += __popc(pm);
+          const long long dl[6] = {d[0], d[1], d[2], d[3], d[4], d[5]};
+          agg_sums(prop, kb + A, dl, true, a.sp.sums, a.sp.dirty, a.stamp);
+          agg_sums(prop, kb + Bm, dl, false, a.sp.sums, a.sp.dirty, a.stamp);
+          if (lane == 0) atomicAdd(&s_cnt[4], __popc(pm));
         } else {
           agg_add_i32(prop, kb + A, (int)d[0], a.sp.out);
           const int np = __popc(pm);
@@ -936,13 +946,8 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
     if (lane < pleft) a.props[pbase + lane] = make_uint4(0u, 0xffffffffu, 0u, 0u);
     if (lane + 32 < pleft) a.props[pbase + lane + 32] = make_uint4(0u, 0xffffffffu, 0u, 0u);
   }
-  if (lane == 0) {
-    if (c_cand) atomicAdd(&a.cnt[0], (unsigned long long)c_cand);
-    if (c_topo) atomicAdd(&a.cnt[1], (unsigned long long)c_topo);
-    if (c_prop) atomicAdd(&a.cnt[2], (unsigned long long)c_prop);
-    if (c_srej) atomicAdd(&a.cnt[3], (unsigned long long)c_srej);
-    if (c_commit) atomicAdd(&a.cnt[4], (unsigned long long)c_commit);
-  }
+  __syncthreads();
+  if (threadIdx.x < 5 && s_cnt[threadIdx.x]) atomicAdd(&a.cnt[threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
 }
 
 // ------------------------------------------------------------------ K5: commit
@@ -1047,16 +1052,22 @@ void launch_eval(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
   else k_eval<false, false><<<grid, K4B_THREADS, 0, s>>>(a);
 }
 
-static int g_sweep_minb = 3;  // RAPID_SWEEP_MINB (2..4): CTAs per SM the register budget targets
+// Register budget per variant (measured): the pixel stage runs best at 4 CTAs/SM (64
+// registers), the block stages at 3 (80; their 64-bit position sums spill at 64).
+// RAPID_SWEEP_MINB=2..4 forces one budget for every stage (A/B testing).
+static int g_sweep_minb = 0;
+
+template <int MB>
+static int sweep_occ() {
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sweep<true, true, MB>, K4B_THREADS, 0);
+  return nb < 1 ? 1 : nb;
+}
 
 int sweep_occupancy() {
   const char *e = getenv("RAPID_SWEEP_MINB");
   if (e && e[0] >= '2' && e[0] <= '4') g_sweep_minb = e[0] - '0';
-  int nb = 0;
-  if (g_sweep_minb == 2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sweep<true, true, 2>, K4B_THREADS, 0);
-  else if (g_sweep_minb == 4) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sweep<true, true, 4>, K4B_THREADS, 0);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_sweep<true, true, 3>, K4B_THREADS, 0);
-  return nb < 1 ? 1 : nb;
+  return g_sweep_minb == 2 ? sweep_occ<2>() : g_sweep_minb == 3 ? sweep_occ<3>() : sweep_occ<4>();
 }
 
 void launch_bset_build(const PhaseArgs &a, const void *tmap, int grid, cudaStream_t s) {
@@ -1087,15 +1098,19 @@ bool launch_merge_adjacency_tma(const MergeArgs &m, const void *tmap, int grid, 
   return true;
 }
 
-void launch_sweep(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
+void launch_sweep(const PhaseArgs &a, bool pixel, int sm_count, cudaStream_t s) {
   const bool gated = a.size_mode != 0;
+  static int occ[5] = {0, 0, 0, 0, 0};
+  const int mb = g_sweep_minb ? g_sweep_minb : (pixel ? 4 : 3);
+  if (!occ[mb]) occ[mb] = mb == 2 ? sweep_occ<2>() : mb == 3 ? sweep_occ<3>() : sweep_occ<4>();
+  const int grid = sm_count * occ[mb];
 #define RAPID_SWEEP_LAUNCH(MB)                                                    \
   if (pixel && gated) k_sweep<true, true, MB><<<grid, K4B_THREADS, 0, s>>>(a);    \
   else if (pixel) k_sweep<true, false, MB><<<grid, K4B_THREADS, 0, s>>>(a);       \
   else if (gated) k_sweep<false, true, MB><<<grid, K4B_THREADS, 0, s>>>(a);       \
   else k_sweep<false, false, MB><<<grid, K4B_THREADS, 0, s>>>(a);
-  if (g_sweep_minb == 2) { RAPID_SWEEP_LAUNCH(2) }
-  else if (g_sweep_minb == 4) { RAPID_SWEEP_LAUNCH(4) }
+  if (mb == 2) { RAPID_SWEEP_LAUNCH(2) }
+  else if (mb == 4) { RAPID_SWEEP_LAUNCH(4) }
   else { RAPID_SWEEP_LAUNCH(3) }
 #undef RAPID_SWEEP_LAUNCH
 }

@@ -695,6 +695,62 @@ __global__ void __launch_bounds__(256) k_transition(const TransArgs a) {
   }
 }
 
+// Dyadic fast path (both stages uniform, b_prev = 2 b_next): the parent of child (x, y) is
+// (x >> 1, y >> 1), so a parent row yields two identical child rows.  Persistent CTAs of 128
+// threads, one tile per iteration; a thread writes 4 children x 2 rows from 2 parent labels.
+__global__ void __launch_bounds__(128) k_transition_dyadic(const TransArgs a) {
+  const StageDev &pv = a.prev, &nx = a.next;
+  const unsigned ntiles = (unsigned)(nx.tiles_x * nx.tiles_y) * (unsigned)a.B;
+  const bool rm = *a.remap_pending != 0u;
+  const bool vec = (nx.nbx & 3) == 0 && (pv.nbx & 1) == 0;
+  const int u = threadIdx.x;
+  for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint32_t rr = fdiv(t, nx.fd_tx), img = fdiv(rr, nx.fd_ty);
+    const int gx = (int)(t - rr * (uint32_t)nx.tiles_x) * TX + 4 * (u & 15);
+    const int gy = (int)(rr - img * (uint32_t)nx.tiles_y) * TY + 2 * (u >> 4);
+    const int kb = (int)img * a.M;
+    int act = 0;
+    if (gy < nx.nby && gx < nx.nbx) {
+      const int32_t *prow = pv.map + ((size_t)img * pv.nby + (gy >> 1)) * pv.nbx;
+      const int px = gx >> 1;
+      int p0, p1 = -1;
+      if (vec) {
+        const int2 pp = *reinterpret_cast<const int2 *>(prow + px);
+        p0 = pp.x;
+        p1 = pp.y;
+      } else {
+        p0 = prow[px];
+        if (px + 1 < pv.nbx) p1 = prow[px + 1];
+      }
+      if (rm && !a.sp.alive[kb + p0]) p0 = a.sp.remap[kb + p0];
+      if (p1 >= 0 && rm && !a.sp.alive[kb + p1]) p1 = a.sp.remap[kb + p1];
+      if (a.gate) act = a.sp.active[kb + p0] | (p1 >= 0 ? a.sp.active[kb + p1] : 0);
+      int32_t *dst = nx.map + ((size_t)img * nx.nby + gy) * nx.nbx + gx;
+      const bool two = gy + 1 < nx.nby;
+      if (vec) {
+        const int4 v = make_int4(p0, p0, p1, p1);
+        *reinterpret_cast<int4 *>(dst) = v;
+        if (two) *reinterpret_cast<int4 *>(dst + nx.nbx) = v;
+      } else {
+        const int l[4] = {p0, p0, p1, p1};
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          if (gx + k < nx.nbx) {
+            dst[k] = l[k];
+            if (two) dst[nx.nbx + k] = l[k];
+          }
+      }
+    }
+    if (a.gate) {
+      act = __syncthreads_or(act);
+      if (threadIdx.x == 0 && act) {
+        const unsigned p = atomicAdd(a.nwork, 1u);
+        a.worklist[p] = (int)t;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ RECOUNT
 template <bool PIXEL>
 __global__ void k_recount(const RecountArgs a) {
@@ -891,7 +947,14 @@ void launch_predict(const PredictArgs &a, int grid, cudaStream_t s, int *nlaunch
 
 void launch_transition(const TransArgs &a, cudaStream_t s) {
   const unsigned ntiles = (unsigned)(a.next.tiles_x * a.next.tiles_y) * (unsigned)a.B;
-  k_transition<<<ntiles, 256, 0, s>>>(a);
+  if (a.prev.uniform && a.next.uniform && a.prev.b == 2 * a.next.b) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    k_transition_dyadic<<<std::min<unsigned>(ntiles, (unsigned)sms * 16), 128, 0, s>>>(a);
+  } else {
+    k_transition<<<ntiles, 256, 0, s>>>(a);
+  }
 }
 
 void launch_recount(const RecountArgs &a, bool pixel, int grid, cudaStream_t s, int *nlaunch) {

@@ -801,25 +801,56 @@ __global__ void k_final_upsample(const FinalArgs a) {
   }
 }
 
-__global__ void k_final_remap(const FinalArgs a) {
+__global__ void __launch_bounds__(128) k_final_remap(const FinalArgs a) {
   // in place on the map of `last` (== labels); merged-away labels only occur in worklist
-  // tiles at gated stages (victims are active superpixels)
+  // tiles at gated stages (victims are active superpixels).  Persistent CTAs, one tile per
+  // iteration; a thread reads 4 consecutive labels of 2 rows (16-B loads when rows allow),
+  // and writes back only labels whose superpixel was merged away.
   if (*a.remap_pending == 0u) return;
   const StageDev &st = a.last;
   const unsigned ntiles = a.worklist ? *a.nwork : (unsigned)(st.tiles_x * st.tiles_y) * (unsigned)a.B;
-  const size_t n = (size_t)ntiles * (TX * TY);
-  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
-       t += (size_t)gridDim.x * blockDim.x) {
-    const unsigned w = (unsigned)(t / (TX * TY));
-    const int off = (int)(t - (size_t)w * (TX * TY));
+  const bool vec = (st.nbx & 3) == 0;
+  const int u = threadIdx.x;
+  for (unsigned w = blockIdx.x; w < ntiles; w += gridDim.x) {
     const uint32_t tile = a.worklist ? (uint32_t)a.worklist[w] : w;
     const uint32_t r = fdiv(tile, st.fd_tx), img = fdiv(r, st.fd_ty);
-    const int gx = (int)(tile - r * (uint32_t)st.tiles_x) * TX + (off % TX);
-    const int gy = (int)(r - img * (uint32_t)st.tiles_y) * TY + (off / TX);
-    if (gx >= st.nbx || gy >= st.nby) continue;
-    const size_t p = ((size_t)img * st.nby + gy) * st.nbx + gx;
-    const int l = a.labels[p];
-    if (!a.sp.alive[img * a.M + l]) a.labels[p] = a.sp.remap[img * a.M + l];
+    const int gx = (int)(tile - r * (uint32_t)st.tiles_x) * TX + 4 * (u & 15);
+    const int gy0 = (int)(r - img * (uint32_t)st.tiles_y) * TY + 2 * (u >> 4);
+    const int kb = (int)img * a.M;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int gy = gy0 + h;
+      if (gy >= st.nby || gx >= st.nbx) continue;
+      int32_t *p = a.labels + ((size_t)img * st.nby + gy) * st.nbx + gx;
+      int l[4];
+      if (vec) {
+        const int4 v = *reinterpret_cast<const int4 *>(p);
+        l[0] = v.x; l[1] = v.y; l[2] = v.z; l[3] = v.w;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; k++) l[k] = gx + k < st.nbx ? p[k] : -1;
+      }
+      bool dirty = false;
+      int last = -1, res = -1;
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        if (l[k] < 0) continue;
+        if (l[k] != last) {
+          last = l[k];
+          res = a.sp.alive[kb + last] ? last : a.sp.remap[kb + last];
+        }
+        dirty |= res != l[k];
+        l[k] = res;
+      }
+      if (!dirty) continue;
+      if (vec) {
+        *reinterpret_cast<int4 *>(p) = make_int4(l[0], l[1], l[2], l[3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          if (gx + k < st.nbx) p[k] = l[k];
+      }
+    }
   }
 }
 
@@ -975,7 +1006,7 @@ void launch_count_window(const StageDev &st, const SpDev &sp, int B, int M, unsi
 void launch_final(const FinalArgs &a, bool upsample, cudaStream_t s) {
   const size_t n = (size_t)a.H * a.W * a.B;
   if (upsample) k_final_upsample<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(a);
-  else k_final_remap<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(a);
+  else k_final_remap<<<148 * 16, 128, 0, s>>>(a);
 }
 
 }  // namespace rapid

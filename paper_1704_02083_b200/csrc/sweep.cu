@@ -1015,13 +1015,21 @@ bool make_label_tmap(void *tmap64B, int32_t *base, int nbx, int nby, int B) {
       return false;
     encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   }
+  // L2 promotion: the 288-B box rows straddle 256-B granules, so 256-B promotion over-fetches
+  // (RAPID_TMA_PROMO=0/64/128/256 for A/B; default 64)
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+  if (const char *e = getenv("RAPID_TMA_PROMO")) {
+    const int v = atoi(e);
+    promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+          : v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+  }
   const cuuint64_t dims[3] = {(cuuint64_t)nbx, (cuuint64_t)nby, (cuuint64_t)B};
   const cuuint64_t strides[2] = {(cuuint64_t)nbx * 4, (cuuint64_t)nbx * nby * 4};
   const cuuint32_t box[3] = {(cuuint32_t)BOXW, (cuuint32_t)BOXH, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode((CUtensorMap *)tmap64B, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, base, dims, strides, box,
                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 

@@ -27,6 +27,7 @@ struct Ctl {  // per-segmentation device control block (zeroed at the start of e
   unsigned int err;
   unsigned int vtotal, deg_total, npairs, atotal;
   unsigned int mflag[2];  // cooperative merge match: pending flags per round parity
+  unsigned int wq[MAXS * MAXSW * 4];  // k_sweep work-queue counters, one per phase
 };
 
 struct StagePlan {
@@ -591,6 +592,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           pa.cy = ph >> 1;
           pa.gating = gating;
           pa.bset = c->use_bset ? (uint32_t *)c->bset.p : nullptr;
+          pa.wq = &ctl->wq[g];
           {  // enough warp iterations to occupy every sweep warp twice (tile count upper bound)
             const size_t words = (size_t)sd[st].tiles_x * sd[st].tiles_y * B * (TY / 2);
             const size_t warps = (size_t)c->sweep_grid * 8;

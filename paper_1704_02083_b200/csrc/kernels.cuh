@@ -27,6 +27,7 @@ struct PhaseArgs {
   uint32_t *victim_any;
   uint32_t *bset;            // boundary sets of the stage (null: full-scan path K4a/K4b)
   int32_t gwords;            // k_sweep: bset words per warp iteration (4..32)
+  unsigned int *wq;          // k_sweep: work-queue counter of this phase (zeroed per call)
 };
 
 struct SnapArgs {

@@ -720,7 +720,14 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
   __syncthreads();
   unsigned long long pbase = 0;  // this warp's reserved proposal slots
   int pleft = 0;
-  for (unsigned g = gw; g < ngroups; g += nw) {
+  (void)gw;
+  (void)nw;
+  // dynamic distribution of the word groups (one returned atomic per group and warp): the
+  // per-group work varies with the boundary density, static striding left a 10 % tail
+  for (unsigned g = 0;;) {
+    if (lane == 0) g = atomicAdd(a.wq, 1u);
+    g = __shfl_sync(FULL, g, 0);
+    if (g >= ngroups) break;
     // ---- this lane's word
     const unsigned q = g * G + (unsigned)lane, w = q >> 3;  // (tile slot, plane row q % 8)
     uint32_t word = 0, wpos = 0, widx = 0;

@@ -484,9 +484,15 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     for (int st = 0; st < nst; st++)
       if (P.st[st].b > 1) leaf = st;
     if (leaf >= 0) {
-      launch_pyramid_leaf(sd[leaf], image, H, W, B, (uint64_t *)c->bsum.p + P.st[leaf].bsum_off, s);
+      int top = leaf;  // coarsest level written by the leaf kernel
+      if (leaf >= 1 && launch_pyramid_leaf24(sd[leaf], sd[leaf - 1], image, H, W, B,
+                                             (uint64_t *)c->bsum.p + P.st[leaf].bsum_off,
+                                             (uint64_t *)c->bsum.p + P.st[leaf - 1].bsum_off, s))
+        top = leaf - 1;
+      else
+        launch_pyramid_leaf(sd[leaf], image, H, W, B, (uint64_t *)c->bsum.p + P.st[leaf].bsum_off, s);
       c->launches++;
-      for (int st = leaf - 1; st >= 0; st--) {
+      for (int st = top - 1; st >= 0; st--) {
         launch_pyramid_up(sd[st], sd[st + 1], B, (uint64_t *)c->bsum.p + P.st[st].bsum_off, s);
         c->launches++;
       }

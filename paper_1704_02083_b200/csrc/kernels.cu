@@ -102,6 +102,47 @@ __global__ void k_pyramid_leaf2(const StageDev st, const uint8_t *__restrict__ i
 }
 
 // K1: coarser stage from its <= 2x2 children (packed fields never overflow: block <= 64^2).
+// Fused leaf for dyadic pyramids (b = 2 leaf, b = 4 parent, both uniform): one thread reads a
+// 8 x 4 pixel patch (four 2x2 blocks in each of two block rows) with 8-B loads and writes the
+// eight b = 2 sums and the two b = 4 sums: the b = 4 level is not re-read from HBM.
+__global__ void k_pyramid_leaf24(const StageDev st, const StageDev up, const uint8_t *__restrict__ image, int H,
+                                 int W, int B, uint64_t *__restrict__ bsum, uint64_t *__restrict__ bsum_up) {
+  const int q = st.nbx / 4;        // thread groups per block-row pair
+  const int npair = st.nby / 2;    // block-row pairs per image
+  const size_t n = (size_t)q * npair * B;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const size_t pr = t / q;  // img * npair + pair
+    const int gx = (int)(t - pr * q) * 4;
+    const int img = (int)(pr / npair), gy = 2 * (int)(pr - (size_t)img * npair);
+    uint64_t o2[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const uint8_t *p0 = image + (((size_t)img * H + 2 * (gy + h)) * W + 2 * gx) * 3;
+      const uint2 *r0 = reinterpret_cast<const uint2 *>(p0);
+      const uint2 *r1 = reinterpret_cast<const uint2 *>(p0 + (size_t)W * 3);
+      const uint2 a[3] = {__ldcs(r0), __ldcs(r0 + 1), __ldcs(r0 + 2)};
+      const uint2 b[3] = {__ldcs(r1), __ldcs(r1 + 1), __ldcs(r1 + 2)};
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        uint32_t sc[3];
+#pragma unroll
+        for (int ch = 0; ch < 3; ch++)
+          sc[ch] = byte_of(a, 6 * j + ch) + byte_of(a, 6 * j + 3 + ch) + byte_of(b, 6 * j + ch) +
+                   byte_of(b, 6 * j + 3 + ch);
+        o2[h][j] = (uint64_t)sc[0] | ((uint64_t)sc[1] << 21) | ((uint64_t)sc[2] << 42);
+      }
+      uint64_t *dst = bsum + ((size_t)img * st.nby + gy + h) * st.nbx + gx;
+      reinterpret_cast<ulonglong2 *>(dst)[0] = make_ulonglong2(o2[h][0], o2[h][1]);
+      reinterpret_cast<ulonglong2 *>(dst)[1] = make_ulonglong2(o2[h][2], o2[h][3]);
+    }
+    // packed fields never carry: each stays < 2^21 up to b = 90
+    const uint64_t u0 = o2[0][0] + o2[0][1] + o2[1][0] + o2[1][1], u1 = o2[0][2] + o2[0][3] + o2[1][2] + o2[1][3];
+    uint64_t *dup = bsum_up + ((size_t)img * up.nby + (gy >> 1)) * up.nbx + (gx >> 1);
+    *reinterpret_cast<ulonglong2 *>(dup) = make_ulonglong2(u0, u1);
+  }
+}
+
 __global__ void k_pyramid_up(const StageDev st, const StageDev ch, int B, uint64_t *__restrict__ bsum) {
   const size_t nper = (size_t)st.nbx * st.nby;
   const size_t n = nper * B;
@@ -167,12 +208,22 @@ __device__ __forceinline__ void make_rec(const SpDev &sp, int k) {
   int32_t mx = 0, my = 0;
   if (n > 0) {
     const unsigned long long twon = 2 * n;
-    // round-half-up(2^F S / n) = floor((2^(F+1) S + n) / 2n)  (A24)
-    c0 = (uint32_t)(((s[1] << (FRAC + 1)) + n) / twon);
-    c1 = (uint32_t)(((s[2] << (FRAC + 1)) + n) / twon);
-    c2 = (uint32_t)(((s[3] << (FRAC + 1)) + n) / twon);
-    mx = (int32_t)(((s[4] << (FRAC + 1)) + n) / twon);
-    my = (int32_t)(((s[5] << (FRAC + 1)) + n) / twon);
+    // round-half-up(2^F S / n) = floor((2^(F+1) S + n) / 2n)  (A24).  Exact quotient from a
+    // double reciprocal estimate (relative error < 2^-50, quotients < 2^25, so the estimate is
+    // within one of the quotient) and one integer correction step each way.
+    const double rcp = 1.0 / (double)twon;
+    auto qdiv = [&](unsigned long long num) -> unsigned long long {
+      long long q = (long long)((double)num * rcp);
+      long long r = (long long)(num - (unsigned long long)q * twon);
+      if (r < 0) { q--; r += (long long)twon; }
+      if (r >= (long long)twon) q++;
+      return (unsigned long long)q;
+    };
+    c0 = (uint32_t)qdiv((s[1] << (FRAC + 1)) + n);
+    c1 = (uint32_t)qdiv((s[2] << (FRAC + 1)) + n);
+    c2 = (uint32_t)qdiv((s[3] << (FRAC + 1)) + n);
+    mx = (int32_t)qdiv((s[4] << (FRAC + 1)) + n);
+    my = (int32_t)qdiv((s[5] << (FRAC + 1)) + n);
   }
   r.mux = mx;
   r.muy = my;
@@ -895,6 +946,16 @@ static int grid_for(size_t n, int threads, int cap = 148 * 16) {
 
 void launch_init_sp(const InitArgs &a, cudaStream_t s) {
   k_init_sp<<<grid_for(a.K, 256), 256, 0, s>>>(a);
+}
+
+bool launch_pyramid_leaf24(const StageDev &st, const StageDev &up, const uint8_t *image, int H, int W, int B,
+                           uint64_t *bsum, uint64_t *bsum_up, cudaStream_t s) {
+  if (!(st.uniform && up.uniform && st.b == 2 && up.b == 4 && W % 8 == 0 && H % 4 == 0 &&
+        ((uintptr_t)image & 7u) == 0))
+    return false;
+  const size_t n = (size_t)(st.nbx / 4) * (st.nby / 2) * B;
+  k_pyramid_leaf24<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(st, up, image, H, W, B, bsum, bsum_up);
+  return true;
 }
 
 void launch_pyramid_leaf(const StageDev &st, const uint8_t *image, int H, int W, int B,

@@ -110,14 +110,19 @@ __global__ void k_pyramid_leaf24(const StageDev st, const StageDev up, const uin
   const int q = st.nbx / 4;        // thread groups per block-row pair
   const int npair = st.nby / 2;    // block-row pairs per image
   const size_t n = (size_t)q * npair * B;
-  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
-       t += (size_t)gridDim.x * blockDim.x) {
-    const size_t pr = t / q;  // img * npair + pair
-    const int gx = (int)(t - pr * q) * 4;
+  const unsigned lane = threadIdx.x & 31u;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  // warp-uniform trip count (the stores below exchange data between lanes)
+  for (size_t base = blockIdx.x * (size_t)blockDim.x + (threadIdx.x & ~31u); base < n; base += stride) {
+    const size_t t = base + lane;
+    const bool valid = t < n;
+    const size_t pr = valid ? t / q : 0;  // img * npair + pair
+    const int gx = valid ? (int)(t - pr * q) * 4 : 0;
     const int img = (int)(pr / npair), gy = 2 * (int)(pr - (size_t)img * npair);
-    uint64_t o2[2][4];
+    uint64_t o2[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
     for (int h = 0; h < 2; h++) {
+      if (!valid) continue;
       const uint8_t *p0 = image + (((size_t)img * H + 2 * (gy + h)) * W + 2 * gx) * 3;
       const uint2 *r0 = reinterpret_cast<const uint2 *>(p0);
       const uint2 *r1 = reinterpret_cast<const uint2 *>(p0 + (size_t)W * 3);
@@ -132,14 +137,38 @@ __global__ void k_pyramid_leaf24(const StageDev st, const StageDev up, const uin
                    byte_of(b, 6 * j + 3 + ch);
         o2[h][j] = (uint64_t)sc[0] | ((uint64_t)sc[1] << 21) | ((uint64_t)sc[2] << 42);
       }
-      uint64_t *dst = bsum + ((size_t)img * st.nby + gy + h) * st.nbx + gx;
-      reinterpret_cast<ulonglong2 *>(dst)[0] = make_ulonglong2(o2[h][0], o2[h][1]);
-      reinterpret_cast<ulonglong2 *>(dst)[1] = make_ulonglong2(o2[h][2], o2[h][3]);
     }
-    // packed fields never carry: each stays < 2^21 up to b = 90
-    const uint64_t u0 = o2[0][0] + o2[0][1] + o2[1][0] + o2[1][1], u1 = o2[0][2] + o2[0][3] + o2[1][2] + o2[1][3];
-    uint64_t *dup = bsum_up + ((size_t)img * up.nby + (gy >> 1)) * up.nbx + (gx >> 1);
-    *reinterpret_cast<ulonglong2 *>(dup) = make_ulonglong2(u0, u1);
+    // stores: every store instruction of the warp writes whole 32-B sectors (a half-sector
+    // write costs a DRAM read-modify-write).  When the warp's 32 threads are 32 consecutive
+    // groups of one block-row pair, its output rows are contiguous 1-KB runs: lane i stores the
+    // 16 B at offset 16 i, i.e. pair (i & 1) of lane 16 * half + i / 2.
+    const bool contiguous = base + 31 < n && (base / q) == ((base + 31) / q);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      if (contiguous) {
+        const size_t pr0 = base / q;
+        const int img0 = (int)(pr0 / npair), gy0 = 2 * (int)(pr0 - (size_t)img0 * npair);
+        uint64_t *row = bsum + ((size_t)img0 * st.nby + gy0 + h) * st.nbx + (size_t)(base - pr0 * q) * 4;
+#pragma unroll
+        for (int half = 0; half < 2; half++) {
+          const int src = 16 * half + (int)(lane >> 1);
+          const uint64_t a0 = __shfl_sync(0xffffffffu, o2[h][0], src), a1 = __shfl_sync(0xffffffffu, o2[h][1], src);
+          const uint64_t a2 = __shfl_sync(0xffffffffu, o2[h][2], src), a3 = __shfl_sync(0xffffffffu, o2[h][3], src);
+          const bool hi = lane & 1u;
+          *reinterpret_cast<ulonglong2 *>(row + 4 * (size_t)src + (hi ? 2 : 0)) =
+              hi ? make_ulonglong2(a2, a3) : make_ulonglong2(a0, a1);
+        }
+      } else if (valid) {
+        uint64_t *dst = bsum + ((size_t)img * st.nby + gy + h) * st.nbx + gx;
+        reinterpret_cast<ulonglong2 *>(dst)[0] = make_ulonglong2(o2[h][0], o2[h][1]);
+        reinterpret_cast<ulonglong2 *>(dst)[1] = make_ulonglong2(o2[h][2], o2[h][3]);
+      }
+    }
+    if (valid) {  // packed fields never carry: each stays < 2^21 up to b = 90
+      const uint64_t u0 = o2[0][0] + o2[0][1] + o2[1][0] + o2[1][1], u1 = o2[0][2] + o2[0][3] + o2[1][2] + o2[1][3];
+      uint64_t *dup = bsum_up + ((size_t)img * up.nby + (gy >> 1)) * up.nbx + (gx >> 1);
+      *reinterpret_cast<ulonglong2 *>(dup) = make_ulonglong2(u0, u1);
+    }
   }
 }
 

@@ -64,6 +64,19 @@ def workload_for_rank(cfg, rank):
     return w
 
 
+def max_over_ranks(x: float) -> float:
+    """Max of a per-rank float over the process group (identity without one).  NCCL groups
+    reduce a CUDA tensor, gloo groups (the CPU tests) a host tensor."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def peaks():
     try:
         with open(MEASURED) as f:
@@ -254,10 +267,7 @@ def run_ours(args):
     total_launches = int(pr.total_launches)
     _, info = r.stats(0)
 
-    t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(dev_ms)
     px_total = w.pixels * world * args.steps
     value = px_total / (ms_max / 1e3) / 1e6
 
@@ -281,10 +291,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         e_ms = ee0.elapsed_time(ee1)
         wall = (time.perf_counter() - e0) * 1e3
-        te = torch.tensor([max(e_ms, wall)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": round(w.pixels * world * args.steps / (float(te.item()) / 1e3) / 1e6, 3),
+        te = max_over_ranks(max(e_ms, wall))
+        e2e = {"value": round(w.pixels * world * args.steps / (te / 1e3) / 1e6, 3),
                "unit": "Mpixel/s", "h2d_bytes_per_step": w.pixels * 3, "d2h_bytes_per_step": w.pixels * 4,
                "api": "rapid_segment_host (pinned host buffers)"}
         r.set_profiling(1)

@@ -183,6 +183,40 @@ __device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[
   }
 }
 
+// Packed variant for blocks of at most 4 x 4 pixels (b <= 4): one move's data and any 32-lane
+// run sum fit two 64-bit words without a field overflowing into the next — n (10 bits;
+// <= 16 x 32), colour sums (18 bits each; <= 255 x 16 x 32), position sums (26 bits each;
+// <= 2^20 x 32) — so the segmented scan moves 2 words instead of 6.
+__device__ __forceinline__ void agg_sums_small(bool valid, int key, const long long d[6], bool negate,
+                                               unsigned long long *sums, uint32_t *dirty, uint32_t stamp) {
+  if (__ballot_sync(FULL, valid) == 0u) return;  // warp-uniform
+  const WarpRun run = warp_runs(valid, key);
+  const int lane = lane_id();
+  unsigned long long u0 = 0, u1 = 0;
+  if (valid) {
+    u0 = (unsigned long long)d[0] | ((unsigned long long)d[1] << 10) | ((unsigned long long)d[2] << 28) |
+         ((unsigned long long)d[3] << 46);
+    u1 = (unsigned long long)d[4] | ((unsigned long long)d[5] << 26);
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t0 = __shfl_up_sync(FULL, u0, o), t1 = __shfl_up_sync(FULL, u1, o);
+    if (lane - o >= run.start) {
+      u0 += t0;
+      u1 += t1;
+    }
+  }
+  if (valid && run.end) {
+    const long long tot[6] = {(long long)(u0 & 0x3FFull), (long long)((u0 >> 10) & 0x3FFFFull),
+                              (long long)((u0 >> 28) & 0x3FFFFull), (long long)(u0 >> 46),
+                              (long long)(u1 & 0x3FFFFFFull), (long long)(u1 >> 26)};
+    unsigned long long *s = sums + (size_t)key * SUMW;
+#pragma unroll
+    for (int f = 0; f < 6; f++) red_add_keep(&s[f], (unsigned long long)(negate ? -tot[f] : tot[f]));
+    if (dirty != nullptr) dirty[key] = stamp;
+  }
+}
+
 // Warp-aggregated int32 add (proposal outflow per source superpixel); v in [0, 2^16).
 __device__ __forceinline__ void agg_add_i32(bool valid, int key, int v, int32_t *arr) {
   if (__ballot_sync(FULL, valid) == 0u) return;  // warp-uniform

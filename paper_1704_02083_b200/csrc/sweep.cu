@@ -927,8 +927,13 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
             bset_insert(a.bset, st, img, gx, gy, ins);
           }
           const long long dl[6] = {d[0], d[1], d[2], d[3], d[4], d[5]};
-          agg_sums(prop, kb + A, dl, true, a.sp.sums, a.sp.dirty, a.stamp);
-          agg_sums(prop, kb + Bm, dl, false, a.sp.sums, a.sp.dirty, a.stamp);
+          if (PIXEL || st.b <= 4) {  // warp-uniform
+            agg_sums_small(prop, kb + A, dl, true, a.sp.sums, a.sp.dirty, a.stamp);
+            agg_sums_small(prop, kb + Bm, dl, false, a.sp.sums, a.sp.dirty, a.stamp);
+          } else {
+            agg_sums(prop, kb + A, dl, true, a.sp.sums, a.sp.dirty, a.stamp);
+            agg_sums(prop, kb + Bm, dl, false, a.sp.sums, a.sp.dirty, a.stamp);
+          }
           if (lane == 0) atomicAdd(&s_cnt[4], __popc(pm));
         } else {
           agg_add_i32(prop, kb + A, (int)d[0], a.sp.out);
@@ -999,8 +1004,13 @@ __global__ void __launch_bounds__(256) k_commit(const PhaseArgs a) {
         }
       }
     }
-    agg_sums(ok, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp);
-    agg_sums(ok, kb + B, d, false, a.sp.sums, a.sp.dirty, a.stamp);
+    if (PIXEL || a.st.b <= 4) {  // warp-uniform
+      agg_sums_small(ok, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp);
+      agg_sums_small(ok, kb + B, d, false, a.sp.sums, a.sp.dirty, a.stamp);
+    } else {
+      agg_sums(ok, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp);
+      agg_sums(ok, kb + B, d, false, a.sp.sums, a.sp.dirty, a.stamp);
+    }
     c_commit += __popc(__ballot_sync(FULL, ok));
     c_rej += __popc(__ballot_sync(FULL, rej));
   }

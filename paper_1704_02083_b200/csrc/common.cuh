@@ -190,7 +190,6 @@ __device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[
 __device__ __forceinline__ void agg_sums_small(bool valid, int key, const long long d[6], bool negate,
                                                unsigned long long *sums, uint32_t *dirty, uint32_t stamp) {
   if (__ballot_sync(FULL, valid) == 0u) return;  // warp-uniform
-  const WarpRun run = warp_runs(valid, key);
   const int lane = lane_id();
   unsigned long long u0 = 0, u1 = 0;
   if (valid) {
@@ -198,15 +197,22 @@ __device__ __forceinline__ void agg_sums_small(bool valid, int key, const long l
          ((unsigned long long)d[3] << 46);
     u1 = (unsigned long long)d[4] | ((unsigned long long)d[5] << 26);
   }
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long t0 = __shfl_up_sync(FULL, u0, o), t1 = __shfl_up_sync(FULL, u1, o);
-    if (lane - o >= run.start) {
+  // group the lanes by key (not only adjacent runs): the group's lowest lane gathers the
+  // others' words with shuffles (iterations = largest group - 1) and issues the atomics
+  const unsigned grp = __match_any_sync(FULL, valid ? key : -1 - lane);
+  const bool leader = valid && (__ffs(grp) - 1) == lane;
+  unsigned rem = leader ? grp & ~(1u << lane) : 0u;
+  const unsigned long long v0 = u0, v1 = u1;
+  while (__any_sync(FULL, rem != 0u)) {
+    const int src = rem ? __ffs(rem) - 1 : lane;
+    const unsigned long long t0 = __shfl_sync(FULL, v0, src), t1 = __shfl_sync(FULL, v1, src);
+    if (rem) {
       u0 += t0;
       u1 += t1;
+      rem &= rem - 1;
     }
   }
-  if (valid && run.end) {
+  if (leader) {
     const long long tot[6] = {(long long)(u0 & 0x3FFull), (long long)((u0 >> 10) & 0x3FFFFull),
                               (long long)((u0 >> 28) & 0x3FFFFull), (long long)(u0 >> 46),
                               (long long)(u1 & 0x3FFFFFFull), (long long)(u1 >> 26)};

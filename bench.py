@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--setting", default="rapid", choices=list(synth.SETTINGS),
+                    help="SURVEY f1 comparison setting (rapid = the headline workload)")
     ap.add_argument("--sample", type=int, default=8192, help="side of the bounded CPU sample (~7 s of oracle work)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -57,8 +59,8 @@ def dist_env():
     return rank, world, local
 
 
-def workload_for_rank(cfg, rank):
-    w = synth.config(cfg)
+def workload_for_rank(cfg, rank, setting="rapid"):
+    w = synth.with_setting(synth.config(cfg), setting)
     if rank:
         w.seeds = [s + 1000 * rank for s in w.seeds]
     return w
@@ -101,9 +103,9 @@ def config_dict(w, extra=None):
 
 
 # ----------------------------------------------------------------------------- CPU oracle
-def oracle_sample(cfg, side, seed_offset=0):
+def oracle_sample(cfg, side, seed_offset=0, setting="rapid"):
     import oracle
-    sw = synth.scaled(cfg, side, side, seed_offset=seed_offset)
+    sw = synth.with_setting(synth.scaled(cfg, side, side, seed_offset=seed_offset), setting)
     img = sw.images()
     t0 = time.perf_counter()
     oracle.segment(img, sw.params)
@@ -111,8 +113,8 @@ def oracle_sample(cfg, side, seed_offset=0):
     return sw, dt
 
 
-def cpu_baseline(cfg, side):
-    sw, dt = oracle_sample(cfg, side)
+def cpu_baseline(cfg, side, setting="rapid"):
+    sw, dt = oracle_sample(cfg, side, setting=setting)
     return {"value": round(sw.pixels / dt / 1e6, 4), "unit": "Mpixel/s", "cores": 1, "kind": "oracle",
             "sample": f"{sw.name}: {side}x{side} px with config {cfg}'s densities and parameters, "
                       f"full pipeline, single-threaded C oracle, {dt:.2f} s"}
@@ -122,10 +124,10 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    w = synth.config(args.config)
+    w = synth.with_setting(synth.config(args.config), args.setting)
     times = []
     for i in range(args.warmup + args.steps):
-        sw, dt = oracle_sample(args.config, args.sample, seed_offset=0)
+        sw, dt = oracle_sample(args.config, args.sample, seed_offset=0, setting=args.setting)
         if i >= args.warmup:
             times.append(dt)
     px = sw.pixels
@@ -214,7 +216,7 @@ def run_ours(args):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    w = workload_for_rank(args.config, rank)
+    w = workload_for_rank(args.config, rank, args.setting)
     p = w.params
     t0 = time.time()
     host = torch.empty((w.B, w.H, w.W, 3), dtype=torch.uint8).pin_memory()
@@ -347,9 +349,12 @@ def run_ours(args):
                      "phase_set", "eval"])},
                 "stage_sweep_ms": [round(float(x), 3) for x in prof_ms[rb.K_PROPOSE][:len(p.block_sizes)]],
                 "stage_sweeps_run": [int(x) for x in info.stage_sweeps_run[:len(p.block_sizes)]],
+                "stage_candidates": [int(cnt[s, :, :, rb.C_CAND].sum()) for s in range(len(p.block_sizes))],
+                "stage_commits": [int(cnt[s, :, :, rb.C_COMMIT].sum()) for s in range(len(p.block_sizes))],
+                "setting": args.setting,
                 "alive": int(info.alive), "active": int(info.active)}
         if not args.no_cpu:
-            line["cpu_baseline"] = cpu_baseline(args.config, args.sample)
+            line["cpu_baseline"] = cpu_baseline(args.config, args.sample, args.setting)
         print(json.dumps(line), flush=True)
     r.close()
     if world > 1:

@@ -177,3 +177,26 @@ def scaled(k: int, H: int, W: int, B: int = 1, seed_offset: int = 0) -> Workload
     nuclei = [round(base.nuclei[0] * frac)] * B
     return Workload(f"{base.name}_sample{H}x{W}x{B}", B, H, W, seeds, regions, nuclei,
                     base.bg_permille, p)
+
+
+# the paper's comparison settings on this path (Table 1).  They
+# only configure the existing kernels (run_ctftps / run_multiscale / run_rapid).
+SETTINGS = ("rapid", "ctftps", "multiscale")
+
+
+def with_setting(w: Workload, setting: str) -> Workload:
+    """Copy of workload `w` under one of SETTINGS: RAPID = the config's own parameters;
+    CTFTPS = HARD size bound, no mask, REUSE; multi-scale CTFTPS = the same with statistics
+    recounted at every stage (RECOUNT)."""
+    import copy
+    if setting not in SETTINGS:
+        raise ValueError(setting)
+    w2 = copy.deepcopy(w)
+    if setting == "rapid":  # the config's own parameters (configs 3-5: MERGE + CLASS + REUSE)
+        return w2
+    p = w2.params
+    p.size_mode, p.mask_rule = SIZE_HARD, MASK_OFF
+    p.stats_mode = STATS_RECOUNT if setting == "multiscale" else STATS_REUSE
+    w2.name = f"{w.name}_{setting}"
+    return w2
+

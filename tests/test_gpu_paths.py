@@ -80,3 +80,21 @@ def test_graph_replay_follows_inputs_and_params():
         assert np.array_equal(labels.cpu().numpy(), oracle.segment(img2, p2).labels)
     finally:
         r.close()
+
+
+@pytest.mark.parametrize("setting", synth.SETTINGS)
+def test_comparison_settings_oracle_exact(setting):
+    """CTFTPS (HARD, no mask), multi-scale CTFTPS (+ RECOUNT) and RAPID (MERGE +
+    CLASS + REUSE) on a 768^2 sample with config 4's densities, bit-exact with the oracle."""
+    w = synth.with_setting(synth.scaled(4, 768, 768), setting)
+    img = w.images()
+    ref = oracle.segment(img, w.params)
+    r = make_ctx({}, w.pixels, w.params.n_superpixels)
+    try:
+        lab, sp, info = gpu_run(r, img, w.params)
+    finally:
+        r.close()
+    assert np.array_equal(lab, ref.labels)
+    assert np.array_equal(sp["n"], ref.sp["n"])
+    assert info.status == 0
+    assert np.array_equal(info.counters()[..., oracle.C_COMMIT], ref.counters[..., oracle.C_COMMIT])

@@ -716,7 +716,13 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
   const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const int colour = a.cx | (a.cy << 1);
   __shared__ unsigned s_cnt[5];  // cand, topo, prop, srej, commit (per CTA; flushed at the end)
+  __shared__ uint32_t s_simple[8];  // 256-bit truth table of simple_point (E_topo) by ring mask
   if (threadIdx.x < 5) s_cnt[threadIdx.x] = 0u;
+  {
+    static_assert(K4B_THREADS == 256, "one thread per ring mask");
+    const unsigned t = __ballot_sync(FULL, simple_point(threadIdx.x));
+    if ((threadIdx.x & 31) == 0) s_simple[threadIdx.x >> 5] = t;
+  }
   __syncthreads();
   unsigned long long pbase = 0;  // this warp's reserved proposal slots
   int pleft = 0;
@@ -808,7 +814,7 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
                               ((unsigned)(dSE == A) << 3) | ((unsigned)(nq2 == A) << 4) |
                               ((unsigned)(dSW == A) << 5) | ((unsigned)(nq3 == A) << 6) |
                               ((unsigned)(dNW == A) << 7);
-          const bool topo_ok = simple_point(m8);
+          const bool topo_ok = (s_simple[m8 >> 5] >> (m8 & 31u)) & 1u;
           // distinct candidate labels (A8), compacted: cb[0..nb) with the slot mask cm of each;
           // maskA = slots labelled A.  Records: first 16 B (means + flags).
           int cb[4] = {0, 0, 0, 0};

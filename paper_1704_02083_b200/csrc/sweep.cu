@@ -793,11 +793,14 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
         const size_t o = (size_t)gy * nbx + gx;
         const bool hN = gy > 0, hS = gy + 1 < nby, hW = gx > 0, hE = gx + 1 < nbx;
         // streaming loads (evict-first): keep L2 for the per-superpixel tables
-        A = __ldcs(m + o);
-        const int nq0 = hN ? __ldcs(m + o - nbx) : -1, nq1 = hE ? __ldcs(m + o + 1) : -1;
-        const int nq2 = hS ? __ldcs(m + o + nbx) : -1, nq3 = hW ? __ldcs(m + o - 1) : -1;
-        const int dNE = hN && hE ? __ldcs(m + o - nbx + 1) : -1, dSE = hS && hE ? __ldcs(m + o + nbx + 1) : -1;
-        const int dSW = hS && hW ? __ldcs(m + o + nbx - 1) : -1, dNW = hN && hW ? __ldcs(m + o - nbx - 1) : -1;
+#ifndef RAPID_WLD
+#define RAPID_WLD __ldcs
+#endif
+        A = RAPID_WLD(m + o);
+        const int nq0 = hN ? RAPID_WLD(m + o - nbx) : -1, nq1 = hE ? RAPID_WLD(m + o + 1) : -1;
+        const int nq2 = hS ? RAPID_WLD(m + o + nbx) : -1, nq3 = hW ? RAPID_WLD(m + o - 1) : -1;
+        const int dNE = hN && hE ? RAPID_WLD(m + o - nbx + 1) : -1, dSE = hS && hE ? RAPID_WLD(m + o + nbx + 1) : -1;
+        const int dSW = hS && hW ? RAPID_WLD(m + o + nbx - 1) : -1, dNW = hN && hW ? RAPID_WLD(m + o - nbx - 1) : -1;
         const int nq[4] = {nq0, nq1, nq2, nq3};
         const bool bnd = (nq0 >= 0 && nq0 != A) | (nq1 >= 0 && nq1 != A) | (nq2 >= 0 && nq2 != A) |
                          (nq3 >= 0 && nq3 != A);

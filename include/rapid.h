@@ -159,6 +159,18 @@ int rapid_segment(rapid_ctx *ctx, const uint8_t *image, int32_t H, int32_t W,
 int rapid_segment_host(rapid_ctx *ctx, const uint8_t *image_host, int32_t H, int32_t W,
                        const rapid_params *params, int32_t *labels_host, void *stream);
 
+/* A stream of n independent segmentations from host buffers, all with the same H, W and
+ * params: images_host[k] (u8 [B][H][W][3]) -> labels_host[k] (int32 [B][H][W]), k = 0..n-1.
+ * Equivalent to n rapid_segment_host calls, but pipelined over two device buffer pairs and
+ * two copy streams: the labels of segmentation k travel to the host while the image of k+1
+ * is copied in and segmented (copies of each direction stay in order; host buffers should be
+ * pinned for the copies to overlap).  Segmentations run on `stream`; returns after every
+ * label buffer is written, with the first error status of any of them (RAPID_E_INTEGRITY when
+ * a RECOUNT check failed).  rapid_stats afterwards reports the last segmentation.
+ * Errors: RAPID_E_ARG (n < 1, a null buffer), otherwise as rapid_segment_host. */
+int rapid_segment_host_stream(rapid_ctx *ctx, const uint8_t *const *images_host, int32_t *const *labels_host,
+                              int32_t n, int32_t H, int32_t W, const rapid_params *params, void *stream);
+
 /* Synchronise the last segmentation's stream and copy per-superpixel stats (up to
  * `capacity` entries; out_host may be NULL) and run info (may be NULL) to the host.
  * Returns the deferred status of that segmentation (e.g. RAPID_E_INTEGRITY). */

@@ -116,6 +116,8 @@ def _load():
     L.rapid_init.argtypes = [ctypes.POINTER(vp), ctypes.c_int, u64, u64]
     L.rapid_segment.argtypes = [vp, vp, i32, i32, ctypes.POINTER(rapid_params), vp, vp]
     L.rapid_segment_host.argtypes = [vp, vp, i32, i32, ctypes.POINTER(rapid_params), vp, vp]
+    L.rapid_segment_host_stream.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), i32, i32, i32,
+                                            ctypes.POINTER(rapid_params), vp]
     L.rapid_stats.argtypes = [vp, vp, u64, ctypes.POINTER(rapid_run_info)]
     L.rapid_set_profiling.argtypes = [vp, ctypes.c_int]
     L.rapid_get_profile.argtypes = [vp, ctypes.POINTER(rapid_profile)]
@@ -127,15 +129,16 @@ def _load():
     L.rapid_last_error.restype = ctypes.c_char_p
     L.rapid_debug_stop.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
     L.rapid_debug_map.argtypes = [vp, vp, u64, ctypes.POINTER(i32), ctypes.POINTER(i32)]
-    for f in ("rapid_init", "rapid_segment", "rapid_segment_host", "rapid_stats", "rapid_set_profiling",
-              "rapid_get_profile", "rapid_debug_stop", "rapid_debug_map"):
+    for f in ("rapid_init", "rapid_segment", "rapid_segment_host", "rapid_segment_host_stream", "rapid_stats",
+              "rapid_set_profiling", "rapid_get_profile", "rapid_debug_stop", "rapid_debug_map"):
         getattr(L, f).restype = ctypes.c_int
     return L
 
 
 lib = _load()
 
-EXPORTS = ("rapid_init", "rapid_segment", "rapid_segment_host", "rapid_stats", "rapid_set_profiling",
+EXPORTS = ("rapid_init", "rapid_segment", "rapid_segment_host", "rapid_segment_host_stream", "rapid_stats",
+           "rapid_set_profiling",
            "rapid_get_profile", "rapid_free", "rapid_status_string", "rapid_last_error",
            "rapid_debug_stop", "rapid_debug_map")
 
@@ -187,6 +190,15 @@ def rapid_segment(ctx, image_ptr, H, W, params: rapid_params, labels_ptr, stream
 
 def rapid_segment_host(ctx, image_ptr, H, W, params: rapid_params, labels_ptr, stream_ptr):
     rc = lib.rapid_segment_host(ctx, image_ptr, H, W, ctypes.byref(params), labels_ptr, stream_ptr)
+    if rc:
+        raise RapidError(rc, lib.rapid_last_error(ctx).decode())
+
+
+def rapid_segment_host_stream(ctx, image_ptrs, label_ptrs, H, W, params: rapid_params, stream_ptr):
+    n = len(image_ptrs)
+    ia = (ctypes.c_void_p * n)(*image_ptrs)
+    la = (ctypes.c_void_p * n)(*label_ptrs)
+    rc = lib.rapid_segment_host_stream(ctx, ia, la, n, H, W, ctypes.byref(params), stream_ptr)
     if rc:
         raise RapidError(rc, lib.rapid_last_error(ctx).decode())
 
@@ -253,6 +265,20 @@ class Rapid:
         if stream is not None:
             sp = stream.cuda_stream
         rapid_segment_host(self.ctx, img.ctypes.data, H, W, make_params(params, B), labels.ctypes.data, sp)
+        self.last_batch = B
+        return labels
+
+    def segment_host_stream(self, images, params, labels=None, stream=None):
+        """images: list of numpy u8 [B,H,W,3] (host; pin them for overlap) -> list of numpy int32
+        [B,H,W]; pipelined (the labels of k return while k+1 is copied in and segmented)."""
+        imgs = [np.ascontiguousarray(i if i.ndim == 4 else i[None], dtype=np.uint8) for i in images]
+        B, H, W, _ = imgs[0].shape
+        assert all(i.shape == imgs[0].shape for i in imgs), "all images of a stream share one shape"
+        if labels is None:
+            labels = [np.empty((B, H, W), dtype=np.int32) for _ in imgs]
+        sp = 0 if stream is None else stream.cuda_stream
+        rapid_segment_host_stream(self.ctx, [i.ctypes.data for i in imgs], [l.ctypes.data for l in labels], H, W,
+                                  make_params(params, B), sp)
         self.last_batch = B
         return labels
 

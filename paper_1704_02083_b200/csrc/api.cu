@@ -104,7 +104,6 @@ struct rapid_ctx {
   bool use_graph = true;  // RAPID_NO_GRAPH=1 enqueues the kernels one by one (A/B testing)
   bool l2_persist = false;  // RAPID_L2_PERSIST=1: L2 access-policy window on the sums (graph path)
   cudaStream_t cap_stream = nullptr;
-  cudaGraphExec_t gexec = nullptr;
   unsigned plan_gen = 0;
   struct GraphKey {
     const void *image;
@@ -112,7 +111,25 @@ struct rapid_ctx {
     int H, W, prof;
     unsigned plan_gen;
     rapid_params p;
-  } gkey;
+  };
+  struct GraphEntry {  // one captured segmentation; owns the events its profiling nodes record
+    GraphKey key;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<ProfEv> evs;
+    std::vector<cudaEvent_t> owned;
+    int launches = 0;
+    uint64_t used = 0;
+  };
+  static constexpr size_t GRAPH_CACHE = 4;  // e.g. the two buffer pairs of the host stream API
+  std::vector<GraphEntry> gcache;
+  uint64_t gclock = 0;
+  bool capturing = false;
+  std::vector<cudaEvent_t> cap_owned;
+  // host stream API (rapid_segment_host_stream): second buffer pair, copy streams, events
+  DevBuf himg2, hlab2;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t hev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  uint32_t *herr = nullptr;  // pinned: RECOUNT flags of the stream's segmentations
   bool use_tma = true;  // RAPID_NO_TMA=1 forces the LDG tile loader (A/B testing)
   // profiling
   int prof = 0;  // 0 off, 1 events, 2 events + window counting
@@ -424,6 +441,12 @@ struct Timer {  // CUDA events around a launch group (profiling mode only)
     else cudaEventRecord(e, s);
   }
   cudaEvent_t next() {
+    if (c->capturing) {  // events of a captured graph belong to its cache entry
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      c->cap_owned.push_back(e);
+      return e;
+    }
     if (c->ev_used == c->ev_pool.size()) {
       cudaEvent_t e;
       cudaEventCreate(&e);
@@ -764,8 +787,18 @@ void rapid_free(rapid_ctx *c) {
   cudaGetDevice(&prev);
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  for (auto &g : c->gcache) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (cudaEvent_t e : g.owned) cudaEventDestroy(e);
+  }
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
+  for (cudaEvent_t e : c->hev)
+    if (e) cudaEventDestroy(e);
+  if (c->herr) cudaFreeHost(c->herr);
+  for (DevBuf *b : {&c->himg2, &c->hlab2})
+    if (b->p) cudaFree(b->p);
   void *ptrs[] = {c->sums, c->rc, c->rec, c->init, c->out, c->remap, c->head,
                   c->vlist, c->alist, c->pairs, c->alive, c->active, c->victim, c->y, c->dirty,
                   c->deg, c->chunk, c->hkeys, c->candE, c->hvals, c->hnext, c->candT, c->ctl,
@@ -868,10 +901,20 @@ int rapid_segment(rapid_ctx *c, const uint8_t *image, int32_t H, int32_t W, cons
     k.prof = c->prof;
     k.plan_gen = c->plan_gen;
     k.p = *p;
-    if (!c->gexec || memcmp(&k, &c->gkey, sizeof k) != 0) {
-      if (c->gexec) {
-        cudaGraphExecDestroy(c->gexec);
-        c->gexec = nullptr;
+    rapid_ctx::GraphEntry *ent = nullptr;
+    for (auto &g : c->gcache)
+      if (memcmp(&k, &g.key, sizeof k) == 0) ent = &g;
+    if (!ent) {
+      if (c->gcache.size() == rapid_ctx::GRAPH_CACHE) {  // evict the least recently used
+        auto old = std::min_element(c->gcache.begin(), c->gcache.end(),
+                                    [](const rapid_ctx::GraphEntry &x, const rapid_ctx::GraphEntry &y) {
+                                      return x.used < y.used;
+                                    });
+        cudaStreamSynchronize(c->last_stream);
+        cudaDeviceSynchronize();
+        if (old->exec) cudaGraphExecDestroy(old->exec);
+        for (cudaEvent_t e : old->owned) cudaEventDestroy(e);
+        c->gcache.erase(old);
       }
       if (!c->cap_stream) {
         if ((rc = cuda_check(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking), "capture stream")))
@@ -900,23 +943,44 @@ int rapid_segment(rapid_ctx *c, const uint8_t *image, int32_t H, int32_t W, cons
       if ((rc = cuda_check(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal),
                            "begin capture")))
         return rc;
+      c->capturing = true;
+      c->cap_owned.clear();
       rc = enqueue(c, image, H, W, p, labels_out, c->cap_stream);
+      c->capturing = false;
       cudaGraph_t g = nullptr;
       const cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g);
+      auto drop_events = [&]() {
+        for (cudaEvent_t ev : c->cap_owned) cudaEventDestroy(ev);
+        c->cap_owned.clear();
+      };
       if (rc) {
         if (g) cudaGraphDestroy(g);
+        drop_events();
         return rc;
       }
-      if ((rc = cuda_check(c, e, "end capture"))) return rc;
-      const cudaError_t ei = cudaGraphInstantiate(&c->gexec, g, 0);
+      if ((rc = cuda_check(c, e, "end capture"))) {
+        drop_events();
+        return rc;
+      }
+      rapid_ctx::GraphEntry ne;
+      const cudaError_t ei = cudaGraphInstantiate(&ne.exec, g, 0);
       cudaGraphDestroy(g);
       if ((rc = cuda_check(c, ei, "graph instantiate"))) {
-        c->gexec = nullptr;
+        drop_events();
         return rc;
       }
-      c->gkey = k;
+      ne.key = k;
+      ne.evs = c->evs;
+      ne.owned = c->cap_owned;
+      ne.launches = c->launches;
+      c->cap_owned.clear();
+      c->gcache.push_back(ne);
+      ent = &c->gcache.back();
     }
-    rc = cuda_check(c, cudaGraphLaunch(c->gexec, s), "graph launch");
+    ent->used = ++c->gclock;
+    c->evs = ent->evs;  // the profile of this call = the events of this graph
+    c->launches = ent->launches;
+    rc = cuda_check(c, cudaGraphLaunch(ent->exec, s), "graph launch");
   } else {
     rc = enqueue(c, image, H, W, p, labels_out, s);
   }
@@ -947,6 +1011,64 @@ int rapid_segment_host(rapid_ctx *c, const uint8_t *image_host, int32_t H, int32
   unsigned err = 0;
   cudaMemcpy(&err, &c->ctl->err, 4, cudaMemcpyDeviceToHost);
   return err ? fail(c, RAPID_E_INTEGRITY, "RECOUNT mismatch") : RAPID_OK;
+}
+
+int rapid_segment_host_stream(rapid_ctx *c, const uint8_t *const *images, int32_t *const *labels, int32_t n,
+                              int32_t H, int32_t W, const rapid_params *p, void *stream) {
+  if (!c) return RAPID_E_ARG;
+  if (!images || !labels || n < 1) return fail(c, RAPID_E_ARG, "null buffer list or n < 1");
+  for (int k = 0; k < n; k++)
+    if (!images[k] || !labels[k]) return fail(c, RAPID_E_ARG, "null host buffer");
+  int rc = validate(c, H, W, p);
+  if (rc) return rc;
+  cudaSetDevice(c->device);
+  const size_t px = (size_t)p->batch * H * W;
+  if ((rc = ensure(c, c->himg, px * 3)) || (rc = ensure(c, c->hlab, px * 4)) ||
+      (rc = ensure(c, c->himg2, px * 3)) || (rc = ensure(c, c->hlab2, px * 4)))
+    return rc;
+  if (!c->h2d) {
+    if ((rc = cuda_check(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking), "h2d stream")) ||
+        (rc = cuda_check(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking), "d2h stream")))
+      return rc;
+    for (cudaEvent_t &e : c->hev)
+      if ((rc = cuda_check(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "stream events"))) return rc;
+    if ((rc = cuda_check(c, cudaMallocHost(&c->herr, 64 * sizeof(uint32_t)), "pinned flags"))) return rc;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  uint8_t *dimg[2] = {(uint8_t *)c->himg.p, (uint8_t *)c->himg2.p};
+  int32_t *dlab[2] = {(int32_t *)c->hlab.p, (int32_t *)c->hlab2.p};
+  cudaEvent_t *in_done = c->hev, *seg_done = c->hev + 2, *out_done = c->hev + 4;
+  // every event starts "complete" so that the first two segmentations need not wait
+  for (cudaEvent_t e : c->hev) cudaEventRecord(e, s);
+  uint32_t err_any = 0;
+  for (int k = 0; k < n; k++) {
+    const int b = k & 1;
+    // image k -> buffer b, once segmentation k-2 has read it
+    cudaStreamWaitEvent(c->h2d, seg_done[b], 0);
+    cudaMemcpyAsync(dimg[b], images[k], px * 3, cudaMemcpyHostToDevice, c->h2d);
+    cudaEventRecord(in_done[b], c->h2d);
+    // segment k once its image is in and the labels of k-2 have left buffer b
+    cudaStreamWaitEvent(s, in_done[b], 0);
+    cudaStreamWaitEvent(s, out_done[b], 0);
+    if ((rc = rapid_segment(c, dimg[b], H, W, p, dlab[b], stream))) break;
+    cudaMemcpyAsync(&c->herr[k & 63], &c->ctl->err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+    cudaEventRecord(seg_done[b], s);
+    // labels k -> host while k+1 is copied in and segmented
+    cudaStreamWaitEvent(c->d2h, seg_done[b], 0);
+    cudaMemcpyAsync(labels[k], dlab[b], px * 4, cudaMemcpyDeviceToHost, c->d2h);
+    cudaEventRecord(out_done[b], c->d2h);
+    if ((k & 63) == 63) {  // drain the pinned flag ring
+      cudaStreamSynchronize(s);
+      for (int j = 0; j < 64; j++) err_any |= c->herr[j];
+    }
+  }
+  const int rs = cuda_check(c, cudaStreamSynchronize(s), "host stream segment");
+  const int r2 = cuda_check(c, cudaStreamSynchronize(c->d2h), "host stream d2h");
+  if (rc) return rc;
+  if (rs) return rs;
+  if (r2) return r2;
+  for (int j = 0; j < (n & 63); j++) err_any |= c->herr[j];
+  return err_any ? fail(c, RAPID_E_INTEGRITY, "RECOUNT mismatch") : RAPID_OK;
 }
 
 int rapid_stats(rapid_ctx *c, rapid_sp_stat *out, uint64_t capacity, rapid_run_info *info) {

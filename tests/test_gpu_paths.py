@@ -98,3 +98,28 @@ def test_comparison_settings_oracle_exact(setting):
     assert np.array_equal(sp["n"], ref.sp["n"])
     assert info.status == 0
     assert np.array_equal(info.counters()[..., oracle.C_COMMIT], ref.counters[..., oracle.C_COMMIT])
+
+
+@pytest.mark.parametrize("stats_mode", [0, 1])
+def test_host_stream_api_pipelined_oracle_exact(stats_mode):
+    """rapid_segment_host_stream: n host images through two device buffer pairs and two copy
+    streams; every output equals the oracle (also with RECOUNT integrity checks on)."""
+    import torch
+    n = 5
+    ws = [synth.scaled(3, 384, 384, seed_offset=k) for k in range(n)]
+    for w in ws:
+        w.params.stats_mode = stats_mode
+    imgs = []
+    for w in ws:
+        h = torch.empty((1, w.H, w.W, 3), dtype=torch.uint8).pin_memory()
+        w.images(out=h.numpy())
+        imgs.append(h.numpy())
+    labs = [torch.empty((1, ws[0].H, ws[0].W), dtype=torch.int32).pin_memory().numpy() for _ in range(n)]
+    r = make_ctx({}, ws[0].pixels, ws[0].params.n_superpixels)
+    try:
+        r.segment_host_stream(imgs, ws[0].params, labs)
+    finally:
+        r.close()
+    for k in range(n):
+        ref = oracle.segment(imgs[k], ws[0].params)
+        assert np.array_equal(labs[k], ref.labels), f"image {k}"

@@ -1,0 +1,43 @@
+"""Measure every BASELINE.json config on one GPU: GPU Mpx/s per segmentation (bench.py), the
+sweep roofline fraction, and the single-threaded oracle's Mpx/s on the same input (configs
+1-3 and 5 in full; config 4 on its 8192^2 density-matched sample).  Prints a markdown table.
+
+    python tools/all_configs.py > profiles/<round>_all_configs.md
+"""
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402  (test infrastructure: the CPU baseline leg only)
+import synth  # noqa: E402
+
+rows = []
+for cfg in (1, 2, 3, 4, 5):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", str(cfg), "--steps", "10",
+                          "--warmup", "3", "--no-e2e", "--no-cpu"], capture_output=True, text=True, check=True)
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    if cfg == 4:
+        w = synth.scaled(4, 8192, 8192)
+        what = "8192² sample"
+    else:
+        w = synth.config(cfg)
+        what = "full"
+    img = w.images()
+    t0 = time.perf_counter()
+    oracle.segment(img, w.params)
+    dt = time.perf_counter() - t0
+    rows.append((cfg, d, w.pixels / dt / 1e6, what, dt))
+
+print("| config | workload | GPU ms / segmentation | GPU Mpx/s | k_sweep frac (pixel stage) | "
+      "phase-set frac | oracle Mpx/s (1 core) | oracle input |")
+print("|---|---|---|---|---|---|---|---|")
+for cfg, d, omp, what, dt in rows:
+    c = d["config"]
+    print(f"| {cfg} | {c['batch']}×{c['H']}×{c['W']}, M={c['superpixels_per_image']}, {c['size_mode']}/{c['mask_rule']} | "
+          f"{d['ms_per_step']:.3f} | {d['value']:.0f} | {d['roofline']['frac']:.3f} | "
+          f"{d['roofline']['phase_set']['frac']:.3f} | {omp:.2f} | {what} ({dt:.1f} s) |")

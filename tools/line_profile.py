@@ -44,7 +44,8 @@ def line_map(func):
 
 def main(rep, kregex, func, top=40):
     lm = line_map(func)
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kregex}"],
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kregex}",
+                          "--launch-count", "1"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     hdr = next(r for r in rows if "Address" in r)

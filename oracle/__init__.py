@@ -19,6 +19,29 @@ C_CAND, C_TOPO, C_PROP, C_SIZEREJ, C_COMMIT, C_COMMREJ = range(6)
 STOP_NONE, STOP_PHASE, STOP_STAGE_START, STOP_AFTER_MERGE, STOP_AFTER_PREDICT = range(5)
 
 
+class OrcQuality(ctypes.Structure):
+    _fields_ = [("pixels", ctypes.c_int64), ("leak", ctypes.c_int64), ("gt_boundary", ctypes.c_int64),
+                ("covered", ctypes.c_int64)]
+
+
+def quality(labels, gt, eps=2):
+    """f4: under-segmentation error and boundary recall of labels [B][H][W] against the
+    ground-truth segment map gt (same shape).  Returns dict(ue, br, pixels, leak, gt_boundary,
+    covered); br = 1.0 when gt has no boundary pixel."""
+    lab = np.ascontiguousarray(labels, dtype=np.int32)
+    g = np.ascontiguousarray(gt, dtype=np.int32)
+    if lab.ndim == 2:
+        lab, g = lab[None], g[None]
+    assert lab.shape == g.shape
+    B, H, W = lab.shape
+    q = OrcQuality()
+    rc = lib().orc_quality_eval(lab.ctypes.data, g.ctypes.data, B, H, W, int(eps), ctypes.byref(q))
+    if rc:
+        raise ValueError(f"orc_quality_eval failed ({rc})")
+    return {"ue": q.leak / q.pixels, "br": (q.covered / q.gt_boundary) if q.gt_boundary else 1.0,
+            "pixels": q.pixels, "leak": q.leak, "gt_boundary": q.gt_boundary, "covered": q.covered}
+
+
 class OrcParams(ctypes.Structure):
     _fields_ = [
         ("n_superpixels", ctypes.c_int32),
@@ -109,6 +132,9 @@ def lib():
                                      ctypes.POINTER(OrcParams), ctypes.POINTER(ctypes.c_int32),
                                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_uint64)]
         L.orc_block_move.restype = ctypes.c_int
+        L.orc_quality_eval.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int, ctypes.POINTER(OrcQuality)]
+        L.orc_quality_eval.restype = ctypes.c_int
         _LIB = L
     return _LIB
 

@@ -795,3 +795,82 @@ int orc_segment(const uint8_t *image, int B, int H, int W, const orc_params *p,
   }
   return ORC_OK;
 }
+
+/* ===================================================================== f4: quality
+ * Plain definitions (oracle.h).  UE: the (superpixel, segment) intersection sizes by sorting
+ * the per-pixel pairs; superpixel sizes by sorting the labels.  BR: direct window scan. */
+static int cmp_u64(const void *a, const void *b) {
+  const uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+static int is_boundary(const int32_t *m, int H, int W, int x, int y) {
+  const int32_t v = m[(size_t)y * W + x];
+  if (x > 0 && m[(size_t)y * W + x - 1] != v) return 1;
+  if (x + 1 < W && m[(size_t)y * W + x + 1] != v) return 1;
+  if (y > 0 && m[(size_t)(y - 1) * W + x] != v) return 1;
+  if (y + 1 < H && m[(size_t)(y + 1) * W + x] != v) return 1;
+  return 0;
+}
+
+int orc_quality_eval(const int32_t *labels, const int32_t *gt, int B, int H, int W, int eps, orc_quality *out) {
+  if (!labels || !gt || !out || B < 1 || H < 1 || W < 1 || eps < 0) return ORC_E_ARG;
+  const size_t n = (size_t)H * W;
+  uint64_t *pairs = (uint64_t *)malloc(sizeof(uint64_t) * n);
+  uint64_t *sps = (uint64_t *)malloc(sizeof(uint64_t) * n);
+  if (!pairs || !sps) {
+    free(pairs);
+    free(sps);
+    return ORC_E_OOM;
+  }
+  memset(out, 0, sizeof *out);
+  out->pixels = (int64_t)B * (int64_t)n;
+  for (int b = 0; b < B; b++) {
+    const int32_t *L = labels + (size_t)b * n, *G = gt + (size_t)b * n;
+    for (size_t i = 0; i < n; i++) {
+      if (L[i] < 0 || G[i] < 0) {
+        free(pairs);
+        free(sps);
+        return ORC_E_ARG;
+      }
+      pairs[i] = ((uint64_t)(uint32_t)L[i] << 32) | (uint32_t)G[i];
+      sps[i] = (uint32_t)L[i];
+    }
+    qsort(pairs, n, sizeof(uint64_t), cmp_u64);
+    qsort(sps, n, sizeof(uint64_t), cmp_u64);
+    /* walk the pairs; |sp| by binary search of the sorted labels */
+    size_t i = 0;
+    while (i < n) {
+      size_t j = i;
+      while (j < n && pairs[j] == pairs[i]) j++;
+      const uint64_t sp = pairs[i] >> 32;
+      size_t lo = 0, hi = n;  /* first index with sps >= sp */
+      while (lo < hi) {
+        const size_t mid = (lo + hi) / 2;
+        if (sps[mid] < sp) lo = mid + 1; else hi = mid;
+      }
+      size_t e = lo;
+      while (e < n && sps[e] == sp) e++;
+      const int64_t inter = (int64_t)(j - i), size = (int64_t)(e - lo);
+      const int64_t rest = size - inter;
+      out->leak += inter < rest ? inter : rest;
+      i = j;
+    }
+    for (int y = 0; y < H; y++)
+      for (int x = 0; x < W; x++) {
+        if (!is_boundary(G, H, W, x, y)) continue;
+        out->gt_boundary++;
+        int hit = 0;
+        for (int dy = -eps; dy <= eps && !hit; dy++)
+          for (int dx = -eps; dx <= eps && !hit; dx++) {
+            const int xx = x + dx, yy = y + dy;
+            if (xx >= 0 && yy >= 0 && xx < W && yy < H && is_boundary(L, H, W, xx, yy)) hit = 1;
+          }
+        out->covered += hit;
+      }
+  }
+  free(pairs);
+  free(sps);
+  return ORC_OK;
+}
+

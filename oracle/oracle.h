@@ -111,4 +111,17 @@ void orc_round_mean(int64_t S, int64_t n, int64_t *q);              /* O5 */
 /* O6 steps 2-6 for one block in isolation (see oracle.c) */
 int orc_block_move(const int32_t *win, const int64_t *means, const int64_t *d, const int64_t *e,
                    const orc_params *p, int32_t *B_out, int64_t *dE_hi, uint64_t *dE_lo);
+/* segmentation quality against a ground-truth segment map (the
+ * standard metrics of "Peer"; definitions as SPEC §Operations states them in words).
+ * labels, gt: int32 [B][H][W], per-image ids >= 0; each image is scored on its own and the
+ * counts are summed over the batch.
+ *   UE: leak = sum over images, GT segments S and superpixels sp meeting S of
+ *       min(|sp n S|, |sp \ S|);  UE = leak / (B H W).
+ *   BR(eps): a pixel is a boundary pixel of a map if one of its in-image 4-neighbours has
+ *       another id; BR = (#GT boundary pixels with a superpixel boundary pixel within
+ *       Chebyshev distance eps) / (#GT boundary pixels), 1 when there is none. */
+typedef struct {
+  int64_t pixels, leak, gt_boundary, covered;
+} orc_quality;
+int orc_quality_eval(const int32_t *labels, const int32_t *gt, int B, int H, int W, int eps, orc_quality *out);
 #endif

@@ -38,6 +38,8 @@ def _lib():
         lib = ctypes.CDLL(path)
         lib.synth_image.argtypes = [ctypes.POINTER(_SynthParams), ctypes.c_void_p, ctypes.c_int]
         lib.synth_image.restype = ctypes.c_int
+        lib.synth_segments.argtypes = [ctypes.POINTER(_SynthParams), ctypes.c_void_p, ctypes.c_int]
+        lib.synth_segments.restype = ctypes.c_int
         lib.synth_hash.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
         lib.synth_hash.restype = ctypes.c_uint64
         _LIB = lib
@@ -53,6 +55,19 @@ def image(H, W, seed, n_regions, n_nuclei, bg_permille=0, noise_sigma=8, nthread
     rc = _lib().synth_image(ctypes.byref(p), out.ctypes.data, nthreads)
     if rc != 0:
         raise ValueError(f"synth_image failed ({rc})")
+    return out
+
+
+def segments(H, W, seed, n_regions, n_nuclei, bg_permille=0, nthreads=0, out=None):
+    """Ground-truth segment map int32 [H][W] of the same generator parameters: tissue region k,
+    background cell n_regions + j, or nucleus n_regions + 64 + k (the blob painted last)."""
+    if out is None:
+        out = np.empty((H, W), dtype=np.int32)
+    assert out.dtype == np.int32 and out.shape == (H, W) and out.flags.c_contiguous
+    p = _SynthParams(seed, H, W, n_regions, n_nuclei, bg_permille, 0)
+    rc = _lib().synth_segments(ctypes.byref(p), out.ctypes.data, nthreads)
+    if rc != 0:
+        raise ValueError(f"synth_segments failed ({rc})")
     return out
 
 
@@ -118,6 +133,15 @@ class Workload:
     @property
     def pixels(self):
         return self.B * self.H * self.W
+
+    def segments(self, nthreads=0, out=None):
+        """Ground-truth segment maps int32 [B][H][W] (per-image ids, see segments())."""
+        if out is None:
+            out = np.empty((self.B, self.H, self.W), dtype=np.int32)
+        for b in range(self.B):
+            segments(self.H, self.W, self.seeds[b], self.regions[b], self.nuclei[b], self.bg_permille, nthreads,
+                     out=out[b])
+        return out
 
     def images(self, nthreads=0, out=None):
         if out is None:

@@ -139,7 +139,10 @@ static const uint8_t COL_NUC[3] = {70, 35, 100};
 
 enum { ST_REG = 1, ST_CLASS = 2, ST_BG = 3, ST_BGPERM = 4, ST_NUC = 5, ST_NOISE = 6 };
 
-int synth_image(const synth_params *p, uint8_t *out, int nthreads) {
+/* One generator for both outputs: the RGB image (out, may be NULL) and the ground-truth
+ * segment map (seg, may be NULL): segment id = tissue region k (0..R-1), background cell
+ * R + j (j < 64), or nucleus R + 64 + k for the blob painted last at the pixel. */
+static int synth_generate(const synth_params *p, uint8_t *out, int32_t *seg, int nthreads) {
   const int H = p->H, W = p->W;
   if (H < 1 || W < 1 || p->n_regions < 1 || p->n_nuclei < 0) return -1;
 #ifdef _OPENMP
@@ -182,15 +185,21 @@ int synth_image(const synth_params *p, uint8_t *out, int nthreads) {
   /* base colours */
 #pragma omp parallel for schedule(dynamic, 4)
   for (int y = 0; y < H; y++) {
-    uint8_t *row = out + (size_t)y * W * 3;
+    uint8_t *row = out ? out + (size_t)y * W * 3 : NULL;
     for (int x = 0; x < W; x++) {
       const uint8_t *c;
-      if (nbg > 0 && isbg[vgrid_nearest(&vb, x, y)]) c = COL_WHITE;
-      else {
+      const int jb = nbg > 0 ? vgrid_nearest(&vb, x, y) : 0;
+      int sid;
+      if (nbg > 0 && isbg[jb]) {
+        c = COL_WHITE;
+        sid = R + jb;
+      } else {
         int k = vgrid_nearest(&vr, x, y);
         c = rcls[k] == 0 ? COL_PINK : (rcls[k] == 1 ? COL_PURPLE : COL_WHITE);
+        sid = k;
       }
-      row[3 * x] = c[0]; row[3 * x + 1] = c[1]; row[3 * x + 2] = c[2];
+      if (row) { row[3 * x] = c[0]; row[3 * x + 1] = c[1]; row[3 * x + 2] = c[2]; }
+      if (seg) seg[(size_t)y * W + x] = sid;
     }
   }
   /* nuclei, painted in index order (sequential: later blobs overwrite earlier) */
@@ -210,15 +219,18 @@ int synth_image(const synth_params *p, uint8_t *out, int nthreads) {
         int64_t dx = x - cx, dy = y - cy;
         int64_t u = dx * cs + dy * sn, v = -dx * sn + dy * cs; /* Q12 */
         if (u * u * b * b + v * v * a * a <= a2b2) {
-          uint8_t *px = out + ((size_t)y * W + x) * 3;
-          px[0] = COL_NUC[0]; px[1] = COL_NUC[1]; px[2] = COL_NUC[2];
+          if (out) {
+            uint8_t *px = out + ((size_t)y * W + x) * 3;
+            px[0] = COL_NUC[0]; px[1] = COL_NUC[1]; px[2] = COL_NUC[2];
+          }
+          if (seg) seg[(size_t)y * W + x] = (int32_t)(R + NB + k);
         }
       }
     }
   }
   /* noise: Irwin-Hall(12) of 16-bit uniforms; sum has mean 12*65535/2, sd 65536*1 (approx) */
   const int64_t sig = p->noise_sigma;
-  if (sig > 0) {
+  if (out && sig > 0) {
 #pragma omp parallel for schedule(static)
     for (int y = 0; y < H; y++) {
       for (int x = 0; x < W; x++) {
@@ -244,6 +256,11 @@ int synth_image(const synth_params *p, uint8_t *out, int nthreads) {
   free(rx); free(ry); free(rcls);
   return 0;
 }
+
+int synth_image(const synth_params *p, uint8_t *out, int nthreads) { return synth_generate(p, out, NULL, nthreads); }
+
+/* ground-truth segment map of the same parameters (int32 [H][W]) */
+int synth_segments(const synth_params *p, int32_t *seg, int nthreads) { return synth_generate(p, NULL, seg, nthreads); }
 
 /* hash helper exposed for configs that derive per-tile parameters (config 5) */
 uint64_t synth_hash(uint64_t seed, uint64_t stream, uint64_t index) { return rnd(seed, stream, index); }

@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--sample", type=int, default=8192, help="side of the bounded CPU sample (~7 s of oracle work)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-quality", action="store_true", help="skip the untimed f4 UE/BR report")
     return ap.parse_args()
 
 
@@ -303,6 +304,17 @@ def run_ours(args):
                       "across consecutive steps)"}
         r.set_profiling(1)
 
+    # segmentation quality of this step's labels against the generator's
+    # ground-truth segments, on the GPU (rapid_quality), untimed
+    quality = None
+    if not args.no_quality and rank == 0:
+        gt = torch.from_numpy(w.segments()).to(dev)
+        r.segment(img, p, labels)
+        quality = {f"eps{e}": {k: (round(v, 6) if isinstance(v, float) else v)
+                               for k, v in r.quality(labels, gt, p.n_superpixels, e).items()} for e in (0, 2)}
+        quality["gt"] = "synth ground truth: tissue Voronoi regions, background cells, nuclei blobs"
+        del gt
+
     if rank == 0:
         peak, peak_src = peaks()
         pb = phase_bytes(info, w, window)
@@ -356,6 +368,7 @@ def run_ours(args):
                 "stage_candidates": [int(cnt[s, :, :, rb.C_CAND].sum()) for s in range(len(p.block_sizes))],
                 "stage_commits": [int(cnt[s, :, :, rb.C_COMMIT].sum()) for s in range(len(p.block_sizes))],
                 "setting": args.setting,
+                "quality": quality,
                 "alive": int(info.alive), "active": int(info.active)}
         if not args.no_cpu:
             line["cpu_baseline"] = cpu_baseline(args.config, args.sample, args.setting)

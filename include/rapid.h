@@ -171,6 +171,26 @@ int rapid_segment_host(rapid_ctx *ctx, const uint8_t *image_host, int32_t H, int
 int rapid_segment_host_stream(rapid_ctx *ctx, const uint8_t *const *images_host, int32_t *const *labels_host,
                               int32_t n, int32_t H, int32_t W, const rapid_params *params, void *stream);
 
+/* segmentation quality (the metrics of the paper's §4.2) of a label
+ * map against a ground-truth segment map, on the GPU.  labels: device int32 [B][H][W],
+ * per-image ids in [0, M); gt: device int32 [B][H][W], per-image segment ids >= 0.  Each
+ * image is scored on its own; counts are summed over the batch:
+ *   UE  = sum over images, segments S and superpixels sp meeting S of
+ *         min(|sp n S|, |sp \ S|), divided by B*H*W (under-segmentation error);
+ *   BR  = (# GT boundary pixels with a superpixel boundary pixel within Chebyshev distance
+ *         eps) / (# GT boundary pixels), 1 when there is none; a boundary pixel of a map is a
+ *         pixel with an in-image 4-neighbour of another id (boundary recall).
+ * Enqueues on `stream`, synchronises it and writes *out_host.  Errors: RAPID_E_ARG (bad
+ * sizes, eps < 0, or an id out of range found on the device), RAPID_E_CAPACITY (more distinct
+ * (superpixel, segment) pairs than the histogram holds: 2^26), RAPID_E_CUDA, RAPID_E_OOM.
+ * The workspace (pair histogram, sizes, one byte per pixel) is allocated on first use. */
+typedef struct {
+  double ue, br;
+  uint64_t pixels, leak_px, gt_boundary_px, covered_px, pairs;
+} rapid_quality_result;
+int rapid_quality(rapid_ctx *ctx, const int32_t *labels, const int32_t *gt, int32_t B, int32_t H, int32_t W,
+                  int32_t M, int32_t eps, rapid_quality_result *out_host, void *stream);
+
 /* Synchronise the last segmentation's stream and copy per-superpixel stats (up to
  * `capacity` entries; out_host may be NULL) and run info (may be NULL) to the host.
  * Returns the deferred status of that segmentation (e.g. RAPID_E_INTEGRITY). */

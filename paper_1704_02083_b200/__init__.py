@@ -107,6 +107,12 @@ class rapid_profile(ctypes.Structure):
         return np.ctypeslib.as_array(self.launches).reshape(NK, MAX_STAGES).copy()
 
 
+class rapid_quality_result(ctypes.Structure):
+    _fields_ = [("ue", ctypes.c_double), ("br", ctypes.c_double), ("pixels", ctypes.c_uint64),
+                ("leak_px", ctypes.c_uint64), ("gt_boundary_px", ctypes.c_uint64), ("covered_px", ctypes.c_uint64),
+                ("pairs", ctypes.c_uint64)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `make lib` or "
@@ -119,6 +125,7 @@ def _load():
     L.rapid_segment_host_stream.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(vp), i32, i32, i32,
                                             ctypes.POINTER(rapid_params), vp]
     L.rapid_stats.argtypes = [vp, vp, u64, ctypes.POINTER(rapid_run_info)]
+    L.rapid_quality.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, ctypes.POINTER(rapid_quality_result), vp]
     L.rapid_set_profiling.argtypes = [vp, ctypes.c_int]
     L.rapid_get_profile.argtypes = [vp, ctypes.POINTER(rapid_profile)]
     L.rapid_free.argtypes = [vp]
@@ -129,7 +136,8 @@ def _load():
     L.rapid_last_error.restype = ctypes.c_char_p
     L.rapid_debug_stop.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
     L.rapid_debug_map.argtypes = [vp, vp, u64, ctypes.POINTER(i32), ctypes.POINTER(i32)]
-    for f in ("rapid_init", "rapid_segment", "rapid_segment_host", "rapid_segment_host_stream", "rapid_stats",
+    for f in ("rapid_init", "rapid_segment", "rapid_segment_host", "rapid_segment_host_stream", "rapid_quality",
+              "rapid_stats",
               "rapid_set_profiling", "rapid_get_profile", "rapid_debug_stop", "rapid_debug_map"):
         getattr(L, f).restype = ctypes.c_int
     return L
@@ -137,7 +145,8 @@ def _load():
 
 lib = _load()
 
-EXPORTS = ("rapid_init", "rapid_segment", "rapid_segment_host", "rapid_segment_host_stream", "rapid_stats",
+EXPORTS = ("rapid_init", "rapid_segment", "rapid_segment_host", "rapid_segment_host_stream", "rapid_quality",
+           "rapid_stats",
            "rapid_set_profiling",
            "rapid_get_profile", "rapid_free", "rapid_status_string", "rapid_last_error",
            "rapid_debug_stop", "rapid_debug_map")
@@ -201,6 +210,14 @@ def rapid_segment_host_stream(ctx, image_ptrs, label_ptrs, H, W, params: rapid_p
     rc = lib.rapid_segment_host_stream(ctx, ia, la, n, H, W, ctypes.byref(params), stream_ptr)
     if rc:
         raise RapidError(rc, lib.rapid_last_error(ctx).decode())
+
+
+def rapid_quality(ctx, labels_ptr, gt_ptr, B, H, W, M, eps, stream_ptr) -> rapid_quality_result:
+    q = rapid_quality_result()
+    rc = lib.rapid_quality(ctx, labels_ptr, gt_ptr, B, H, W, M, eps, ctypes.byref(q), stream_ptr)
+    if rc:
+        raise RapidError(rc, lib.rapid_last_error(ctx).decode())
+    return q
 
 
 def rapid_stats(ctx, out_ptr, capacity, info: rapid_run_info):
@@ -281,6 +298,20 @@ class Rapid:
                                   make_params(params, B), sp)
         self.last_batch = B
         return labels
+
+    def quality(self, labels, gt, M, eps=2, stream=None):
+        """f4: UE / BR of device label maps int32 [B,H,W] (torch, cuda) against device
+        ground-truth segment maps of the same shape; returns a dict."""
+        import torch
+        assert labels.is_cuda and gt.is_cuda and labels.dtype == torch.int32 and gt.dtype == torch.int32
+        lab = labels.contiguous() if labels.dim() == 3 else labels.contiguous()[None]
+        g = gt.contiguous() if gt.dim() == 3 else gt.contiguous()[None]
+        assert lab.shape == g.shape
+        B, H, W = lab.shape
+        st = stream if stream is not None else torch.cuda.current_stream(lab.device)
+        q = rapid_quality(self.ctx, lab.data_ptr(), g.data_ptr(), B, H, W, int(M), int(eps), st.cuda_stream)
+        return {"ue": q.ue, "br": q.br, "pixels": q.pixels, "leak": q.leak_px, "gt_boundary": q.gt_boundary_px,
+                "covered": q.covered_px, "pairs": q.pairs}
 
     def stats(self, K=None):
         info = rapid_run_info()

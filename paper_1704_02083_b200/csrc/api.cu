@@ -130,6 +130,8 @@ struct rapid_ctx {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t hev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   uint32_t *herr = nullptr;  // pinned: RECOUNT flags of the stream's segmentations
+  // f4 quality workspace (rapid_quality)
+  DevBuf qkeys, qcnt, qsize, qspb, qacc;
   bool use_tma = true;  // RAPID_NO_TMA=1 forces the LDG tile loader (A/B testing)
   // profiling
   int prof = 0;  // 0 off, 1 events, 2 events + window counting
@@ -797,7 +799,7 @@ void rapid_free(rapid_ctx *c) {
   for (cudaEvent_t e : c->hev)
     if (e) cudaEventDestroy(e);
   if (c->herr) cudaFreeHost(c->herr);
-  for (DevBuf *b : {&c->himg2, &c->hlab2})
+  for (DevBuf *b : {&c->himg2, &c->hlab2, &c->qkeys, &c->qcnt, &c->qsize, &c->qspb, &c->qacc})
     if (b->p) cudaFree(b->p);
   void *ptrs[] = {c->sums, c->rc, c->rec, c->init, c->out, c->remap, c->head,
                   c->vlist, c->alist, c->pairs, c->alive, c->active, c->victim, c->y, c->dirty,
@@ -1069,6 +1071,54 @@ int rapid_segment_host_stream(rapid_ctx *c, const uint8_t *const *images, int32_
   if (r2) return r2;
   for (int j = 0; j < (n & 63); j++) err_any |= c->herr[j];
   return err_any ? fail(c, RAPID_E_INTEGRITY, "RECOUNT mismatch") : RAPID_OK;
+}
+
+int rapid_quality(rapid_ctx *c, const int32_t *labels, const int32_t *gt, int32_t B, int32_t H, int32_t W,
+                  int32_t M, int32_t eps, rapid_quality_result *out, void *stream) {
+  if (!c) return RAPID_E_ARG;
+  if (!labels || !gt || !out || B < 1 || H < 1 || W < 1 || M < 1 || eps < 0)
+    return fail(c, RAPID_E_ARG, "rapid_quality: bad arguments");
+  const uint64_t px = (uint64_t)B * H * W;
+  if (px >= (1ull << 32) || (uint64_t)B * M >= (1ull << 31)) return fail(c, RAPID_E_RANGE, "rapid_quality: sizes");
+  cudaSetDevice(c->device);
+  // pair histogram: at least 2x the pixels of small inputs, 4x the superpixels of large ones
+  size_t cap = 1024;
+  const size_t want = std::min<size_t>(2 * px, std::max<size_t>(8 * (size_t)B * M, 1 << 20));
+  while (cap < want && cap < (1ull << 26)) cap <<= 1;
+  int rc;
+  if ((rc = ensure(c, c->qkeys, cap * 8)) || (rc = ensure(c, c->qcnt, cap * 4)) ||
+      (rc = ensure(c, c->qsize, (size_t)B * M * 4)) || (rc = ensure(c, c->qspb, px)) ||
+      (rc = ensure(c, c->qacc, 5 * 8)))
+    return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaMemsetAsync(c->qkeys.p, 0xff, cap * 8, s);
+  cudaMemsetAsync(c->qcnt.p, 0, cap * 4, s);
+  cudaMemsetAsync(c->qsize.p, 0, (size_t)B * M * 4, s);
+  cudaMemsetAsync(c->qacc.p, 0, 5 * 8, s);
+  QualityArgs a;
+  a.labels = labels;
+  a.gt = gt;
+  a.B = B; a.H = H; a.W = W; a.M = M; a.eps = eps;
+  a.keys = (unsigned long long *)c->qkeys.p;
+  a.cnt = (uint32_t *)c->qcnt.p;
+  a.cmask = cap - 1;
+  a.size = (uint32_t *)c->qsize.p;
+  a.spb = (uint8_t *)c->qspb.p;
+  a.acc = (unsigned long long *)c->qacc.p;
+  launch_quality(a, c->sm_count, s);
+  unsigned long long acc[5] = {0, 0, 0, 0, 0};
+  cudaMemcpyAsync(acc, a.acc, sizeof acc, cudaMemcpyDeviceToHost, s);
+  if ((rc = cuda_check(c, cudaStreamSynchronize(s), "rapid_quality"))) return rc;
+  if (acc[4] & 2ull) return fail(c, RAPID_E_ARG, "rapid_quality: a label outside [0, M) or a negative segment id");
+  if (acc[4] & 1ull) return fail(c, RAPID_E_CAPACITY, "rapid_quality: too many (superpixel, segment) pairs");
+  out->pixels = px;
+  out->leak_px = acc[0];
+  out->gt_boundary_px = acc[1];
+  out->covered_px = acc[2];
+  out->pairs = acc[3];
+  out->ue = (double)acc[0] / (double)px;
+  out->br = acc[1] ? (double)acc[2] / (double)acc[1] : 1.0;
+  return RAPID_OK;
 }
 
 int rapid_stats(rapid_ctx *c, rapid_sp_stat *out, uint64_t capacity, rapid_run_info *info) {

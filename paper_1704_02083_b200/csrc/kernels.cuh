@@ -163,6 +163,18 @@ struct FinalArgs {
   const unsigned int *nwork;
 };
 
+// ---- f4 quality metrics (quality.cu)
+struct QualityArgs {
+  const int32_t *labels, *gt;
+  int32_t B, H, W, M, eps;
+  unsigned long long *keys;  // [cap] pair keys ((img*M + sp) << 32 | gt), QEMPTY = free
+  uint32_t *cnt;             // [cap] pair counts
+  unsigned long long cmask;  // cap - 1
+  uint32_t *size;            // [B*M] superpixel sizes
+  uint8_t *spb;              // [B*H*W] superpixel-boundary flags
+  unsigned long long *acc;   // [5] leak, gt boundary, covered, pairs, error flags
+};
+
 // launch wrappers (all enqueue on `s`)
 void launch_init_sp(const InitArgs &a, cudaStream_t s);
 void launch_pyramid_leaf(const StageDev &st, const uint8_t *image, int H, int W, int B,
@@ -193,6 +205,7 @@ void launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int gri
                         int *nlaunch);
 bool launch_merge_adjacency_tma(const MergeArgs &a, const void *tmap, int grid, cudaStream_t s);
 int tiles_occupancy();
+void launch_quality(const QualityArgs &a, int sms, cudaStream_t s);
 void launch_predict(const PredictArgs &a, int grid, cudaStream_t s, int *nlaunch);
 void launch_transition(const TransArgs &a, cudaStream_t s);
 void launch_recount(const RecountArgs &a, bool pixel, int grid, cudaStream_t s, int *nlaunch);

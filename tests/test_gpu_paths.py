@@ -123,3 +123,41 @@ def test_host_stream_api_pipelined_oracle_exact(stats_mode):
     for k in range(n):
         ref = oracle.segment(imgs[k], ws[0].params)
         assert np.array_equal(labs[k], ref.labels), f"image {k}"
+
+
+@pytest.mark.parametrize("cfg,side,eps", [(1, 0, 0), (1, 0, 2), (3, 512, 2), (5, 0, 1)])
+def test_quality_metrics_match_oracle(cfg, side, eps):
+    """f4: UE and BR of the GPU segmentation against the generator's ground-truth
+    segments, computed by rapid_quality on the GPU, equal the oracle's exact counts."""
+    import torch
+    w = synth.scaled(cfg, side, side) if side else synth.config(cfg)
+    if cfg == 5:
+        w.seeds, w.regions, w.nuclei, w.B = w.seeds[:3], w.regions[:3], w.nuclei[:3], 3
+    img, gt = w.images(), w.segments()
+    r = make_ctx({}, w.pixels, w.B * w.params.n_superpixels)
+    try:
+        lab = r.segment(torch.from_numpy(img).cuda(), w.params)
+        q = r.quality(lab, torch.from_numpy(gt).cuda(), w.params.n_superpixels, eps)
+        ref = oracle.quality(lab.cpu().numpy(), gt, eps)
+    finally:
+        r.close()
+    for k in ("pixels", "leak", "gt_boundary", "covered"):
+        assert q[k] == ref[k], k
+    assert 0.0 <= q["ue"] < 1.0 and 0.0 < q["br"] <= 1.0
+
+
+def test_quality_closed_forms_on_gpu():
+    import torch
+    g = np.zeros((1, 8, 8), np.int32)
+    g[..., 4:] = 1
+    lab = np.zeros((1, 8, 8), np.int32)
+    lab[..., 5:] = 1
+    r = make_ctx({}, 64, 4)
+    try:
+        q0 = r.quality(torch.from_numpy(lab).cuda(), torch.from_numpy(g).cuda(), 2, 0)
+        q1 = r.quality(torch.from_numpy(lab).cuda(), torch.from_numpy(g).cuda(), 2, 1)
+        qi = r.quality(torch.from_numpy(g).cuda(), torch.from_numpy(g).cuda(), 2, 0)
+    finally:
+        r.close()
+    assert q0["ue"] == 0.25 and q0["br"] == 0.5 and q1["br"] == 1.0
+    assert qi["ue"] == 0.0 and qi["br"] == 1.0

@@ -27,14 +27,15 @@ for setting in ("rapid", "ctftps", "multiscale"):
 print(f"# f1 comparison settings, config {a.config} ({rows[0]['config']['H']}x{rows[0]['config']['W']}, "
       f"M = {rows[0]['config']['superpixels_per_image']}), one B200\n")
 print("| setting | size / mask / stats | ms per segmentation | Mpx/s | sweep ms per stage | "
-      "candidates per stage (M) | commits per stage (k) |")
-print("|---|---|---|---|---|---|---|")
+      "candidates per stage (M) | commits per stage (k) | UE | BR (eps 0 / 2) |")
+print("|---|---|---|---|---|---|---|---|---|")
 for d in rows:
     c = d["config"]
     print(f"| {d['setting']} | {c['size_mode']} / {c['mask_rule']} / {c['stats_mode']} | {d['ms_per_step']:.2f} | "
           f"{d['value']:.0f} | {', '.join(f'{x:.2f}' for x in d['stage_sweep_ms'])} | "
           f"{', '.join(f'{x / 1e6:.1f}' for x in d['stage_candidates'])} | "
-          f"{', '.join(f'{x / 1e3:.0f}' for x in d['stage_commits'])} |")
+          f"{', '.join(f'{x / 1e3:.0f}' for x in d['stage_commits'])} | "
+          f"{d['quality']['eps2']['ue']:.4f} | {d['quality']['eps0']['br']:.4f} / {d['quality']['eps2']['br']:.4f} |")
 base = {d["setting"]: d["ms_per_step"] for d in rows}
 print(f"\nRAPID vs CTFTPS: {base['ctftps'] / base['rapid']:.2f}x; RAPID vs multi-scale CTFTPS: "
       f"{base['multiscale'] / base['rapid']:.2f}x (the paper reports 4x and 13x on a 12-core Xeon, "

@@ -67,6 +67,10 @@ extern "C" {
 #define RAPID_STATS_REUSE 0   /* RAPID: coarsest-level sums reused (Eq. 8, exact here) */
 #define RAPID_STATS_RECOUNT 1 /* multi-scale CTFTPS: recount at every stage (checked equal) */
 
+/* how the prediction step (RAPID l.3-4, Eq. 6) computes y of each superpixel */
+#define RAPID_Y_PROTO 0    /* distance of the mean colour to the prototypes (A21) */
+#define RAPID_Y_FEATURES 1 /* linear h_theta on the 4 features of P:271 (A31) */
+
 /* per-phase counters (rapid_run_info.phase) */
 #define RAPID_C_CAND 0    /* gated boundary blocks of the phase colour */
 #define RAPID_C_TOPO 1    /* ... that passed the simple-point test */
@@ -97,7 +101,11 @@ typedef struct {
   uint8_t pad_[4];
   int64_t tau2;              /* y=+1 iff min_k ||c - proto_k||^2 <= tau2 (Eq. 6; intensity^2) */
   uint32_t stats_mode;       /* RAPID_STATS_* */
-  uint32_t pad2_;
+  uint32_t y_model;          /* RAPID_Y_* */
+  /* RAPID_Y_FEATURES: y = +1 iff w[0] 2^16 + sum_i w[i] f_i >= 0 with the features f1..f4 in
+   * Q16 (absolute and comparative brightness, intra- and extra-region dissimilarity; A31)
+   * and w in Q16.16, |w| < 2^31 (a model file's bias and weights, rounded) */
+  int64_t feat_w_q16[5];
 } rapid_params;
 
 /* Per-superpixel result, index img*M + local id. */

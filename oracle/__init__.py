@@ -60,6 +60,8 @@ class OrcParams(ctypes.Structure):
         ("proto", (ctypes.c_int32 * 3) * 4),
         ("tau2", ctypes.c_int64),
         ("stats_mode", ctypes.c_int32),
+        ("y_model", ctypes.c_int32),
+        ("feat_w_q16", ctypes.c_int64 * 5),
     ]
 
 
@@ -158,6 +160,9 @@ def make_params(p) -> OrcParams:
             o.proto[k][ch] = pr[ch]
     o.tau2 = p.tau2
     o.stats_mode = p.stats_mode
+    o.y_model = getattr(p, "y_model", 0)
+    for i, v in enumerate(getattr(p, "feat_w_q16", [0] * 5)):
+        o.feat_w_q16[i] = v
     return o
 
 

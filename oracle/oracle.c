@@ -505,11 +505,92 @@ static int merge_round(seg_t *g, int s) {
 }
 
 /* ------------------------------------------------------------------ O8 -- */
+static int cmp_u64_orc(const void *a, const void *b) {
+  const uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* round-half-up(num / den) for num >= 0, den > 0 */
+static int64_t rhu(i128 num, i128 den) { return (int64_t)((2 * num + den) / (2 * den)); }
+
+/* y from a linear model on the 4 features of P:271 (Q16 fixed point).
+ * Brightness of a pixel = (r+g+b)/3; per superpixel n, S = sum(r+g+b), Q = sum((r+g+b)^2):
+ *   f1 = rhu(2^16 S / (765 n))                     absolute brightness / 255
+ *   f2 = f1 - rhu(2^16 S_img / (765 N_img))         comparative brightness
+ *   f3 = rhu(2^16 (n Q - S^2) / (585225 n^2))       intra-region dissimilarity (variance / 255^2)
+ *   f4 = rhu(sum_q |f1 - f1_q| / deg)               extra-region dissimilarity over the distinct
+ *                                                    4-adjacent superpixels q of the stage map
+ *   y = +1 iff w0 2^16 + sum_i w_i f_i >= 0        (Eq. 6) */
+static void predict_features(seg_t *g) {
+  const orc_params *p = g->p;
+  const stage_t *st = &g->st[g->cur];
+  const int M = g->M;
+  i128 *Q = (i128 *)calloc((size_t)M, sizeof(i128));
+  int64_t *f1 = (int64_t *)calloc((size_t)M, sizeof(int64_t));
+  int64_t *dsum = (int64_t *)calloc((size_t)M, sizeof(int64_t));
+  int64_t *deg = (int64_t *)calloc((size_t)M, sizeof(int64_t));
+  const size_t nb = (size_t)st->nbx * st->nby;
+  uint64_t *pairs = (uint64_t *)malloc(sizeof(uint64_t) * (4 * nb + 1));  /* directed adjacent pairs */
+  size_t np = 0;
+  /* Q by the pixels of every block of the current map */
+  for (int j = 0; j < st->nby; j++)
+    for (int i = 0; i < st->nbx; i++) {
+      const int32_t a = lab(g, i, j);
+      for (int y = st->ys[j]; y < st->ys[j + 1]; y++)
+        for (int x = st->xs[i]; x < st->xs[i + 1]; x++) {
+          const uint8_t *px = g->I + ((size_t)y * g->W + x) * 3;
+          const int64_t s = (int64_t)px[0] + px[1] + px[2];
+          Q[a] += (i128)(s * s);
+        }
+    }
+  i128 Simg = 0, Nimg = 0;
+  for (int k = 0; k < M; k++)
+    if (g->alive[k]) {
+      Simg += (i128)(g->S[(size_t)k * 6 + 1] + g->S[(size_t)k * 6 + 2] + g->S[(size_t)k * 6 + 3]);
+      Nimg += (i128)g->S[(size_t)k * 6];
+    }
+  const int64_t fimg = rhu(Simg << 16, 765 * Nimg);
+  for (int k = 0; k < M; k++)
+    if (g->alive[k]) {
+      const i128 n = g->S[(size_t)k * 6], S = g->S[(size_t)k * 6 + 1] + g->S[(size_t)k * 6 + 2] + g->S[(size_t)k * 6 + 3];
+      f1[k] = rhu(S << 16, 765 * n);
+    }
+  for (int j = 0; j < st->nby; j++)
+    for (int i = 0; i < st->nbx; i++) {
+      const int32_t a = lab(g, i, j);
+      for (int dir = 0; dir < 2; dir++) {
+        const int32_t b = lab(g, i + (dir == 0), j + (dir == 1));
+        if (b < 0 || b == a) continue;
+        pairs[np++] = ((uint64_t)(uint32_t)a << 32) | (uint32_t)b;
+        pairs[np++] = ((uint64_t)(uint32_t)b << 32) | (uint32_t)a;
+      }
+    }
+  qsort(pairs, np, sizeof(uint64_t), cmp_u64_orc);
+  for (size_t t = 0; t < np; t++) {
+    if (t > 0 && pairs[t] == pairs[t - 1]) continue;  /* each distinct neighbour once */
+    const int32_t u = (int32_t)(pairs[t] >> 32), v = (int32_t)(pairs[t] & 0xffffffffu);
+    deg[u]++;
+    dsum[u] += f1[u] > f1[v] ? f1[u] - f1[v] : f1[v] - f1[u];
+  }
+  for (int k = 0; k < M; k++) {
+    if (!g->alive[k]) { g->y[k] = 0; continue; }
+    const i128 n = g->S[(size_t)k * 6], S = g->S[(size_t)k * 6 + 1] + g->S[(size_t)k * 6 + 2] + g->S[(size_t)k * 6 + 3];
+    const int64_t f2 = f1[k] - fimg;
+    const int64_t f3 = rhu((n * Q[k] - S * S) << 16, 585225 * n * n);
+    const int64_t f4 = deg[k] ? rhu(dsum[k], deg[k]) : 0;
+    const i128 h = ((i128)p->feat_w_q16[0] << 16) + (i128)p->feat_w_q16[1] * f1[k] + (i128)p->feat_w_q16[2] * f2 +
+                   (i128)p->feat_w_q16[3] * f3 + (i128)p->feat_w_q16[4] * f4;
+    g->y[k] = h >= 0 ? 1 : -1;
+  }
+  free(Q); free(f1); free(dsum); free(deg); free(pairs);
+}
+
 static void predict(seg_t *g) {
   const orc_params *p = g->p;
   const stage_t *st = &g->st[g->cur];
   snapshot(g);
-  for (int k = 0; k < g->M; k++) {
+  if (p->y_model == 1) predict_features(g);
+  for (int k = 0; k < g->M && p->y_model != 1; k++) {
     if (!g->alive[k]) { g->y[k] = 0; g->active[k] = 0; continue; }
     i128 dmin = -1;
     for (int t = 0; t < p->n_proto; t++) {
@@ -765,7 +846,8 @@ static int check_params(int B, int H, int W, const orc_params *p) {
     if (p->l_num < 0 || p->l_den <= 0 || p->l_num >= p->l_den) return ORC_E_ARG;
     if (p->u_den <= 0 || p->u_num <= p->u_den) return ORC_E_ARG;
   }
-  if (p->mask_rule != ORC_MASK_OFF && (p->n_proto < 1 || p->n_proto > 4)) return ORC_E_ARG;
+  if (p->mask_rule != ORC_MASK_OFF && p->y_model == 0 && (p->n_proto < 1 || p->n_proto > 4)) return ORC_E_ARG;
+  if (p->y_model < 0 || p->y_model > 1) return ORC_E_ARG;
   if (p->tau2 < 0) return ORC_E_ARG;
   return ORC_OK;
 }

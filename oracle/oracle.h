@@ -48,6 +48,8 @@ typedef struct {
   int32_t proto[4][3];               /* RGB prototypes for h_theta (A21) */
   int64_t tau2;                      /* y=+1 iff min_k ||c-proto_k||^2 <= tau2 */
   int32_t stats_mode;                /* ORC_STATS_* (A23) */
+  int32_t y_model;                   /* 0: prototype distance (A21); 1: linear model on features (A31) */
+  int64_t feat_w_q16[5];             /* bias, w1..w4 (Q16.16) of the feature model */
 } orc_params;
 
 typedef struct {

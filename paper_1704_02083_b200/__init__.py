@@ -49,7 +49,8 @@ class rapid_params(ctypes.Structure):
         ("pad_", ctypes.c_uint8 * 4),
         ("tau2", ctypes.c_int64),
         ("stats_mode", ctypes.c_uint32),
-        ("pad2_", ctypes.c_uint32),
+        ("y_model", ctypes.c_uint32),
+        ("feat_w_q16", ctypes.c_int64 * 5),
     ]
 
 
@@ -179,6 +180,9 @@ def make_params(p, batch=1) -> rapid_params:
             o.proto_rgb[k][ch] = pr[ch]
     o.tau2 = p.tau2
     o.stats_mode = p.stats_mode
+    o.y_model = getattr(p, "y_model", 0)
+    for i, v in enumerate(getattr(p, "feat_w_q16", [0] * 5)):
+        o.feat_w_q16[i] = v
     return o
 
 

@@ -81,6 +81,11 @@ def hash3(seed, stream, index):
 SIZE_NONE, SIZE_HARD, SIZE_MERGE = 0, 1, 2
 MASK_OFF, MASK_CLASS, MASK_BSP, MASK_EQ7 = 0, 1, 2, 3
 STATS_REUSE, STATS_RECOUNT = 0, 1
+Y_PROTO, Y_FEATURES = 0, 1
+# SURVEY f2 default linear model (training is out of scope; a hand-set model file): tissue
+# (pink / purple) is darker than the white background, y = +1 iff 0.85 - f1 >= 0, i.e. mean
+# brightness <= 0.85 * 255.  Bias, w1..w4 in Q16.16.
+FEAT_W_TISSUE = (round(0.85 * 65536), -65536, 0, 0, 0)
 
 PROTO_PINK = (230, 170, 200)
 PROTO_PURPLE = (120, 70, 150)
@@ -113,6 +118,8 @@ class Params:
     protos: list = field(default_factory=lambda: [PROTO_PINK, PROTO_PURPLE])
     tau2: int = TAU2
     stats_mode: int = STATS_REUSE
+    y_model: int = Y_PROTO
+    feat_w_q16: list = field(default_factory=lambda: list(FEAT_W_TISSUE))
 
     def asdict(self):
         return asdict(self)

@@ -44,8 +44,9 @@ def test_binding_struct_layout_matches_header(built, tmp_path):
 #include "rapid.h"
 int main(void) {
   printf("%zu %zu %zu %zu\n", sizeof(rapid_params), sizeof(rapid_sp_stat), sizeof(rapid_run_info), sizeof(rapid_profile));
-  printf("%zu %zu %zu %zu %zu\n", offsetof(rapid_params, lambda_pos_q16), offsetof(rapid_params, proto_rgb),
-         offsetof(rapid_params, tau2), offsetof(rapid_params, stats_mode), offsetof(rapid_run_info, phase));
+  printf("%zu %zu %zu %zu %zu %zu %zu\n", offsetof(rapid_params, lambda_pos_q16), offsetof(rapid_params, proto_rgb),
+         offsetof(rapid_params, tau2), offsetof(rapid_params, stats_mode), offsetof(rapid_run_info, phase),
+         offsetof(rapid_params, feat_w_q16), sizeof(rapid_quality_result));
   return 0;
 }
 ''')
@@ -58,7 +59,8 @@ int main(void) {
                      ctypes.sizeof(rb.rapid_run_info), ctypes.sizeof(rb.rapid_profile)]
     assert offs == [rb.rapid_params.lambda_pos_q16.offset, rb.rapid_params.proto_rgb.offset,
                     rb.rapid_params.tau2.offset, rb.rapid_params.stats_mode.offset,
-                    rb.rapid_run_info.phase.offset]
+                    rb.rapid_run_info.phase.offset, rb.rapid_params.feat_w_q16.offset,
+                    ctypes.sizeof(rb.rapid_quality_result)]
 
 
 def test_init_without_gpu_fails_loudly(built):

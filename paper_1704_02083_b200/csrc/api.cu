@@ -42,8 +42,8 @@ struct Plan {
   int B = 0, H = 0, W = 0, M = 0, nst = 0;
   int bs[MAXS] = {0};
   int rows = 0, cols = 0;
-  std::vector<int32_t> X, Y, cellx, celly, bxp, byp;
-  size_t o_X = 0, o_Y = 0, o_cellx = 0, o_celly = 0, o_bxp = 0, o_byp = 0;
+  std::vector<int32_t> X, Y, cellx, celly, bxp, byp, b0x, b0y;
+  size_t o_X = 0, o_Y = 0, o_cellx = 0, o_celly = 0, o_bxp = 0, o_byp = 0, o_b0x = 0, o_b0y = 0;
   StagePlan st[MAXS];
   std::vector<int32_t> tab;
   size_t bsum_total = 0;   // uint64 elements
@@ -279,8 +279,13 @@ int validate(rapid_ctx *c, int H, int W, const rapid_params *p) {
       return fail(c, RAPID_E_ARG, "u must be > 1");
   }
   if (p->mask_rule > 3) return fail(c, RAPID_E_ARG, "mask_rule");
-  if (p->mask_rule != RAPID_MASK_OFF && (p->n_proto < 1 || p->n_proto > RAPID_MAX_PROTO))
+  if (p->y_model > RAPID_Y_FEATURES) return fail(c, RAPID_E_ARG, "y_model");
+  if (p->mask_rule != RAPID_MASK_OFF && p->y_model == RAPID_Y_PROTO &&
+      (p->n_proto < 1 || p->n_proto > RAPID_MAX_PROTO))
     return fail(c, RAPID_E_ARG, "mask needs 1..4 prototypes");
+  for (int k = 0; k < 5; k++)
+    if (p->feat_w_q16[k] <= -(1ll << 31) || p->feat_w_q16[k] >= (1ll << 31))
+      return fail(c, RAPID_E_RANGE, "feature weights out of (-2^31, 2^31)");
   if (p->tau2 < 0 || p->tau2 >= (1ll << 40)) return fail(c, RAPID_E_RANGE, "tau2 out of [0, 2^40)");
   if (p->stats_mode > 1) return fail(c, RAPID_E_ARG, "stats_mode");
   const uint64_t px = (uint64_t)p->batch * H * W;
@@ -339,6 +344,8 @@ int build_plan(rapid_ctx *c, int H, int W, const rapid_params *p) {
     for (int y = 0; y <= H; y++) py[y] = y;
     N.bxp = parents(SL.xs, px);
     N.byp = parents(SL.ys, py);
+    N.b0x = parents(S0.xs, px);  // pixel -> stage-0 block (f2 features)
+    N.b0y = parents(S0.ys, py);
   }
   N.o_X = append(N.tab, N.X);
   N.o_Y = append(N.tab, N.Y);
@@ -346,6 +353,8 @@ int build_plan(rapid_ctx *c, int H, int W, const rapid_params *p) {
   N.o_celly = append(N.tab, N.celly);
   N.o_bxp = append(N.tab, N.bxp);
   N.o_byp = append(N.tab, N.byp);
+  N.o_b0x = append(N.tab, N.b0x);
+  N.o_b0y = append(N.tab, N.b0y);
   for (int s = 0; s < nst; s++) {
     StagePlan &S = N.st[s];
     S.o_xs = append(N.tab, S.xs);
@@ -736,6 +745,15 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       pr.chunk = c->chunk;
       pr.total = &ctl->atotal;
       pr.alist = c->alist;
+      pr.y_model = (int)p->y_model;
+      for (int k = 0; k < 5; k++) pr.feat_w[k] = p->feat_w_q16[k];
+      pr.image = image;
+      pr.H = H; pr.W = W;
+      pr.b0x = T + P.o_b0x;
+      pr.b0y = T + P.o_b0y;
+      pr.scratch = c->rc;
+      pr.hkeys = c->hkeys;
+      pr.hmask = c->hcap - 1;
       launch_predict(pr, grid_k, s, &c->launches);
       if (stop_at(RAPID_STOP_AFTER_PREDICT, st, 0, 0)) {
         remap_in_place(st);

@@ -689,12 +689,135 @@ __global__ void k_predict_y(const PredictArgs a) {
   }
 }
 
+
+// boundary superpixels: a 4-adjacent superpixel of the other class (P:200)
 __device__ __forceinline__ int resolve(const SpDev &sp, int kb, int l, bool remap) {
   if (remap && !sp.alive[kb + l]) return sp.remap[kb + l];
   return l;
 }
 
-// boundary superpixels: a 4-adjacent superpixel of the other class (P:200)
+// ---------------------------------------------------- f2: feature model of the prediction
+// A31 (oracle.h / oracle.c predict_features): brightness (r+g+b)/3; per superpixel n,
+// S = sum(r+g+b), Q = sum((r+g+b)^2) over its pixels at stage 0 (after the stage-0 merges).
+// scratch[k*SUMW + 0] = Q, + 2 = f1, + 3 = sum |f1 - f1_q|, + 4 = distinct neighbours, + 5 = f3;
+// image totals S, N at scratch[img*M*SUMW + 6 / 7].  Everything exact (integers, round half up).
+__device__ __forceinline__ long long rhu128(__int128 num, __int128 den) {
+  return (long long)((2 * num + den) / (2 * den));
+}
+
+__global__ void k_feat_q(const PredictArgs a) {  // Q per superpixel from the pixels
+  const bool rm = *a.remap_pending != 0u;
+  const StageDev &st = a.st;
+  const size_t nper = (size_t)a.H * a.W, n = nper * a.B;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t base = blockIdx.x * (size_t)blockDim.x; base < n; base += stride) {  // warp-uniform
+    const size_t t = base + threadIdx.x;
+    const bool valid = t < n;
+    int key = 0;
+    unsigned long long v = 0;
+    if (valid) {
+      const int img = (int)(t / nper);
+      const size_t r = t - (size_t)img * nper;
+      const int y = (int)(r / a.W), x = (int)(r - (size_t)y * a.W);
+      const int kb = img * a.M;
+      const int l = resolve(a.sp, kb, st.map[((size_t)img * st.nby + a.b0y[y]) * st.nbx + a.b0x[x]], rm);
+      key = kb + l;
+      const uint8_t *p = a.image + t * 3;
+      const unsigned long long s = (unsigned long long)p[0] + p[1] + p[2];
+      v = s * s;
+    }
+    const WarpRun run = warp_runs(valid, key);
+    const int lane = lane_id();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long u = __shfl_up_sync(FULL, v, o);
+      if (lane - o >= run.start) v += u;
+    }
+    if (valid && run.end) atomicAdd(&a.scratch[(size_t)key * SUMW + 0], v);
+  }
+}
+
+__global__ void k_feat_f1(const PredictArgs a) {  // f1, f3 per superpixel; image totals
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.K; k += gridDim.x * blockDim.x) {
+    if (!a.sp.alive[k]) continue;
+    const unsigned long long *sm = a.sp.sums + (size_t)k * SUMW;
+    const __int128 n = (long long)sm[0], S = (long long)(sm[1] + sm[2] + sm[3]);
+    const __int128 Q = (__int128)a.scratch[(size_t)k * SUMW + 0];
+    const long long f1 = rhu128(S << 16, 765 * n);
+    const long long f3 = rhu128((n * Q - S * S) << 16, 585225 * n * n);
+    a.scratch[(size_t)k * SUMW + 2] = (unsigned long long)f1;
+    a.scratch[(size_t)k * SUMW + 5] = (unsigned long long)f3;
+    const int img = k / a.M;
+    atomicAdd(&a.scratch[(size_t)img * a.M * SUMW + 6], (unsigned long long)(long long)S);
+    atomicAdd(&a.scratch[(size_t)img * a.M * SUMW + 7], (unsigned long long)(long long)n);
+  }
+}
+
+// distinct 4-adjacent superpixel pairs of the stage-0 map: a directed pair (u, v) counts for u
+// once (set insert into the merge hash); f4's sum and degree are accumulated at insertion
+__global__ void k_feat_adj(const PredictArgs a) {
+  const StageDev &st = a.st;
+  const bool rm = *a.remap_pending != 0u;
+  const size_t nper = (size_t)st.nbx * st.nby, n = nper * a.B;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x) {
+    const int img = (int)(t / nper);
+    const size_t r = t - (size_t)img * nper;
+    const int gy = (int)(r / st.nbx), gx = (int)(r - (size_t)gy * st.nbx);
+    const int kb = img * a.M;
+    const int la = kb + resolve(a.sp, kb, st.map[t], rm);
+#pragma unroll
+    for (int dir = 0; dir < 2; dir++) {
+      if (dir == 0 ? gx + 1 >= st.nbx : gy + 1 >= st.nby) continue;
+      const int lb = kb + resolve(a.sp, kb, st.map[t + (dir == 0 ? 1 : st.nbx)], rm);
+      if (lb == la) continue;
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        const int u = e ? lb : la, v = e ? la : lb;
+        const unsigned long long key = ((unsigned long long)(unsigned)u << 32) | (unsigned)v;
+        unsigned long long h = hmix(key) & a.hmask;
+        while (true) {
+          const unsigned long long seen = *reinterpret_cast<volatile unsigned long long *>(&a.hkeys[h]);
+          if (seen == key) break;  // already counted
+          if (seen == HEMPTY) {
+            const unsigned long long old = atomicCAS(&a.hkeys[h], HEMPTY, key);
+            if (old == HEMPTY) {  // first sighting of the pair: count it for u
+              const long long fu = (long long)a.scratch[(size_t)u * SUMW + 2];
+              const long long fv = (long long)a.scratch[(size_t)v * SUMW + 2];
+              atomicAdd(&a.scratch[(size_t)u * SUMW + 3], (unsigned long long)(fu > fv ? fu - fv : fv - fu));
+              atomicAdd(&a.scratch[(size_t)u * SUMW + 4], 1ull);
+              break;
+            }
+            if (old == key) break;
+          }
+          h = (h + 1) & a.hmask;
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_feat_classify(const PredictArgs a) {  // Eq. 6 on the features
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.K; k += gridDim.x * blockDim.x) {
+    if (!a.sp.alive[k]) {
+      a.sp.y[k] = 0;
+      a.sp.active[k] = 0;
+      continue;
+    }
+    const int img = k / a.M;
+    const unsigned long long *ims = a.scratch + (size_t)img * a.M * SUMW;
+    const long long fimg = rhu128((__int128)(long long)ims[6] << 16, (__int128)765 * (long long)ims[7]);
+    const unsigned long long *f = a.scratch + (size_t)k * SUMW;
+    const long long f1 = (long long)f[2], f2 = f1 - fimg, f3 = (long long)f[5];
+    const long long deg = (long long)f[4];
+    const long long f4 = deg ? rhu128((long long)f[3], deg) : 0;
+    const __int128 h = ((__int128)a.feat_w[0] << 16) + (__int128)a.feat_w[1] * f1 + (__int128)a.feat_w[2] * f2 +
+                       (__int128)a.feat_w[3] * f3 + (__int128)a.feat_w[4] * f4;
+    const int8_t y = h >= 0 ? 1 : -1;
+    a.sp.y[k] = y;
+    a.sp.active[k] = (a.mask_rule == 1) ? (y == 1) : 0;
+  }
+}
+
 __global__ void k_predict_bsp(const PredictArgs a) {
   const StageDev &st = a.st;
   const bool rm = *a.remap_pending != 0u;
@@ -1052,8 +1175,20 @@ void launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int gri
 }
 
 void launch_predict(const PredictArgs &a, int grid, cudaStream_t s, int *nlaunch) {
-  k_predict_y<<<grid_for(a.K, 256), 256, 0, s>>>(a);
-  *nlaunch += 1;
+  if (a.y_model == 1) {  // f2: linear model on the superpixel features
+    const size_t npx = (size_t)a.B * a.H * a.W, nb = (size_t)a.st.nbx * a.st.nby * a.B;
+    k_feat_q<<<grid_for(npx, 256, 148 * 16), 256, 0, s>>>(a);
+    k_feat_f1<<<grid_for(a.K, 256), 256, 0, s>>>(a);
+    k_feat_adj<<<grid_for(nb, 256, 148 * 16), 256, 0, s>>>(a);
+    k_feat_classify<<<grid_for(a.K, 256), 256, 0, s>>>(a);
+    // restore the invariants of the borrowed buffers: RECOUNT scratch zero, merge hash empty
+    cudaMemsetAsync(a.scratch, 0, sizeof(unsigned long long) * SUMW * (size_t)a.K, s);
+    cudaMemsetAsync(a.hkeys, 0xff, sizeof(unsigned long long) * (a.hmask + 1), s);
+    *nlaunch += 4;
+  } else {
+    k_predict_y<<<grid_for(a.K, 256), 256, 0, s>>>(a);
+    *nlaunch += 1;
+  }
   if (a.mask_rule != 1) {
     const size_t nb = (size_t)a.st.nbx * a.st.nby * a.B;
     k_predict_bsp<<<grid_for(nb, 256, 148 * 32), 256, 0, s>>>(a);

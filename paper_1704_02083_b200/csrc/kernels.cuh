@@ -121,6 +121,15 @@ struct PredictArgs {
   unsigned int *chunk;
   unsigned int *total;
   int32_t *alist;
+  // f2 feature model (y_model == 1): P:271 features, A31
+  int32_t y_model;
+  long long feat_w[5];           // bias, w1..w4 (Q16.16)
+  const uint8_t *image;
+  int32_t H, W;
+  const int32_t *b0x, *b0y;      // pixel column / row -> stage-0 block
+  unsigned long long *scratch;   // [K][SUMW] zeroed scratch (the RECOUNT buffer)
+  unsigned long long *hkeys;     // the merge hash keys (EMPTY outside merge rounds)
+  unsigned long long hmask;
 };
 
 struct TransArgs {

@@ -212,11 +212,12 @@ def scaled(k: int, H: int, W: int, B: int = 1, seed_offset: int = 0) -> Workload
 
 # the paper's comparison settings on this path (Table 1).  They
 # only configure the existing kernels (run_ctftps / run_multiscale / run_rapid).
-SETTINGS = ("rapid", "ctftps", "multiscale")
+SETTINGS = ("rapid", "ctftps", "multiscale", "rapid_features")
 
 
 def with_setting(w: Workload, setting: str) -> Workload:
     """Copy of workload `w` under one of SETTINGS: RAPID = the config's own parameters;
+    rapid_features = RAPID with the f2 feature-model prediction (FEAT_W_TISSUE);
     CTFTPS = HARD size bound, no mask, REUSE; multi-scale CTFTPS = the same with statistics
     recounted at every stage (RECOUNT)."""
     import copy
@@ -226,6 +227,11 @@ def with_setting(w: Workload, setting: str) -> Workload:
     if setting == "rapid":  # the config's own parameters (configs 3-5: MERGE + CLASS + REUSE)
         return w2
     p = w2.params
+    if setting == "rapid_features":  # f2: the prediction by the feature model (tissue model)
+        p.size_mode, p.mask_rule, p.stats_mode = SIZE_MERGE, MASK_CLASS, STATS_REUSE
+        p.y_model, p.feat_w_q16 = Y_FEATURES, list(FEAT_W_TISSUE)
+        w2.name = f"{w.name}_{setting}"
+        return w2
     p.size_mode, p.mask_rule = SIZE_HARD, MASK_OFF
     p.stats_mode = STATS_RECOUNT if setting == "multiscale" else STATS_REUSE
     w2.name = f"{w.name}_{setting}"

@@ -161,3 +161,26 @@ def test_quality_closed_forms_on_gpu():
         r.close()
     assert q0["ue"] == 0.25 and q0["br"] == 0.5 and q1["br"] == 1.0
     assert qi["ue"] == 0.0 and qi["br"] == 1.0
+
+
+@pytest.mark.parametrize("cfg,side,mask", [(3, 512, 1), (3, 384, 2), (4, 512, 3), (5, 0, 1)])
+def test_feature_model_prediction_oracle_exact(cfg, side, mask):
+    """f2 (A31): prediction by the linear model on the 4 superpixel features — labels,
+    y and active flags bit-exact with the oracle, for every mask rule that uses y."""
+    w = synth.scaled(cfg, side, side) if side else synth.config(cfg)
+    if cfg == 5:
+        w.seeds, w.regions, w.nuclei, w.B = w.seeds[:3], w.regions[:3], w.nuclei[:3], 3
+    p = copy.deepcopy(w.params)
+    p.y_model, p.mask_rule = synth.Y_FEATURES, mask
+    p.feat_w_q16 = [round(0.6 * 65536), -65536, 20000, -90000, 30000]  # every feature matters
+    img = w.images()
+    ref = oracle.segment(img, p)
+    r = make_ctx({}, w.pixels, w.B * p.n_superpixels)
+    try:
+        lab, sp, info = gpu_run(r, img, p)
+    finally:
+        r.close()
+    assert np.array_equal(sp["y"], ref.sp["y"]), f"y differs at {int((sp['y'] != ref.sp['y']).sum())} superpixels"
+    alive = ref.sp["alive"] == 1
+    assert np.array_equal(sp["active"][alive], ref.sp["active"][alive])
+    assert np.array_equal(lab, ref.labels)

@@ -737,19 +737,100 @@ __global__ void k_feat_q(const PredictArgs a) {  // Q per superpixel from the pi
   }
 }
 
+// Q on uniform stage-0 grids (square b0 x b0 blocks, b0 in {8, 16, 32, 64}, W % 8 == 0): a CTA
+// takes a band of b0 rows x 256 columns; a thread reads 8 pixels of a row with 8-B loads
+// (they lie in one block), warps reduce each block's row sums with shuffles and add them in
+// shared memory; one atomic per block and band.
+template <int b0>
+__global__ void __launch_bounds__(256) k_feat_q_band(const PredictArgs a) {
+  __shared__ unsigned long long s_q[32];  // blocks of the band (256 / b0 <= 32)
+  const bool rm = *a.remap_pending != 0u;
+  const StageDev &st = a.st;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int gcols = (a.W + 255) / 256, bands_y = a.H / b0;
+  const unsigned nbands = (unsigned)a.B * bands_y * gcols;
+  const int per = b0 / 8;                // lanes per block in a warp row
+  const int nblk = 256 / b0;             // blocks per band
+  for (unsigned band = blockIdx.x; band < nbands; band += gridDim.x) {
+    const unsigned gx = band % gcols, r2 = band / gcols;
+    const int by = (int)(r2 % bands_y), img = (int)(r2 / bands_y);
+    if (threadIdx.x < 32) s_q[threadIdx.x] = 0ull;
+    __syncthreads();
+    const int x0 = (int)gx * 256 + 8 * lane;
+#pragma unroll
+    for (int row = warp; row < b0; row += 8) {  // b0 / 8 independent rows per warp
+      const int y = by * b0 + row;
+      unsigned long long q = 0;
+      if (x0 < a.W) {
+        const uint2 *p = reinterpret_cast<const uint2 *>(a.image + (((size_t)img * a.H + y) * a.W + x0) * 3);
+        const uint2 v[3] = {__ldcs(p), __ldcs(p + 1), __ldcs(p + 2)};
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          const unsigned long long t = (unsigned long long)byte_of(v, 3 * j) + byte_of(v, 3 * j + 1) + byte_of(v, 3 * j + 2);
+          q += t * t;
+        }
+      }
+      for (int o = 1; o < per; o <<= 1) q += __shfl_xor_sync(FULL, q, o);
+      if ((lane % per) == 0 && x0 < a.W) atomicAdd(&s_q[lane / per], q);
+    }
+    __syncthreads();
+    if (threadIdx.x < nblk) {
+      const int bx = (int)gx * nblk + (int)threadIdx.x;
+      if (bx < st.nbx) {
+        const int kb = img * a.M;
+        const int l = resolve(a.sp, kb, st.map[((size_t)img * st.nby + by) * st.nbx + bx], rm);
+        atomicAdd(&a.scratch[(size_t)(kb + l) * SUMW + 0], s_q[threadIdx.x]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void k_feat_f1(const PredictArgs a) {  // f1, f3 per superpixel; image totals
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < a.K; k += gridDim.x * blockDim.x) {
-    if (!a.sp.alive[k]) continue;
-    const unsigned long long *sm = a.sp.sums + (size_t)k * SUMW;
-    const __int128 n = (long long)sm[0], S = (long long)(sm[1] + sm[2] + sm[3]);
-    const __int128 Q = (__int128)a.scratch[(size_t)k * SUMW + 0];
-    const long long f1 = rhu128(S << 16, 765 * n);
-    const long long f3 = rhu128((n * Q - S * S) << 16, 585225 * n * n);
-    a.scratch[(size_t)k * SUMW + 2] = (unsigned long long)f1;
-    a.scratch[(size_t)k * SUMW + 5] = (unsigned long long)f3;
-    const int img = k / a.M;
-    atomicAdd(&a.scratch[(size_t)img * a.M * SUMW + 6], (unsigned long long)(long long)S);
-    atomicAdd(&a.scratch[(size_t)img * a.M * SUMW + 7], (unsigned long long)(long long)n);
+  // warp-uniform trip count: the image totals are warp-aggregated (one atomic per image run)
+  for (int base = blockIdx.x * blockDim.x; base < a.K; base += gridDim.x * blockDim.x) {
+    const int k = base + (int)threadIdx.x;
+    const bool valid = k < a.K && a.sp.alive[k];
+    long long n = 0, S = 0;
+    if (valid) {
+      const unsigned long long *sm = a.sp.sums + (size_t)k * SUMW;
+      n = (long long)sm[0];
+      S = (long long)(sm[1] + sm[2] + sm[3]);
+      const unsigned long long Q = a.scratch[(size_t)k * SUMW + 0];
+      // f1: S 2^16 < 2^58 and 765 n < 2^42 fit 64 bits
+      const long long f1 = (long long)((2ull * ((unsigned long long)S << 16) + 765ull * n) / (2ull * 765ull * n));
+      long long f3;
+      if (n < (1ll << 20)) {  // n Q and S^2 < 2^60: 64-bit products
+        const unsigned long long var = (unsigned long long)n * Q - (unsigned long long)S * S;
+        const unsigned long long den = 585225ull * n * n;  // < 2^60
+        if (var >> 45) f3 = rhu128((__int128)var << 16, (__int128)den);  // keep 2 var 2^16 + den < 2^64
+        else f3 = (long long)((2 * (var << 16) + den) / (2 * den));
+      } else {
+        f3 = rhu128(((__int128)n * Q - (__int128)S * S) << 16, (__int128)585225 * n * n);
+      }
+      a.scratch[(size_t)k * SUMW + 2] = (unsigned long long)f1;
+      a.scratch[(size_t)k * SUMW + 5] = (unsigned long long)f3;
+    }
+    const int img = valid ? k / a.M : -1;
+    const long long d[6] = {n, S, 0, 0, 0, 0};
+    // run-aggregate over lanes of the same image (fields 0, 1 -> totals N, S)
+    if (__ballot_sync(FULL, valid)) {
+      const WarpRun run = warp_runs(valid, img);
+      const int lane = lane_id();
+      long long vn = d[0], vs = d[1];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long tn = __shfl_up_sync(FULL, vn, o), ts = __shfl_up_sync(FULL, vs, o);
+        if (lane - o >= run.start) {
+          vn += tn;
+          vs += ts;
+        }
+      }
+      if (valid && run.end) {
+        atomicAdd(&a.scratch[(size_t)img * a.M * SUMW + 6], (unsigned long long)vs);
+        atomicAdd(&a.scratch[(size_t)img * a.M * SUMW + 7], (unsigned long long)vn);
+      }
+    }
   }
 }
 
@@ -1177,7 +1258,18 @@ void launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int gri
 void launch_predict(const PredictArgs &a, int grid, cudaStream_t s, int *nlaunch) {
   if (a.y_model == 1) {  // f2: linear model on the superpixel features
     const size_t npx = (size_t)a.B * a.H * a.W, nb = (size_t)a.st.nbx * a.st.nby * a.B;
-    k_feat_q<<<grid_for(npx, 256, 148 * 16), 256, 0, s>>>(a);
+    const int b0 = a.st.b;
+    if (a.st.uniform && (b0 == 8 || b0 == 16 || b0 == 32 || b0 == 64) && a.W % 8 == 0 && a.H % b0 == 0 &&
+        a.W % b0 == 0 && ((uintptr_t)a.image & 7u) == 0) {
+      const size_t nbands = (size_t)a.B * (a.H / b0) * ((a.W + 255) / 256);
+      const int g = (int)std::min<size_t>(nbands, 148 * 8);
+      if (b0 == 8) k_feat_q_band<8><<<g, 256, 0, s>>>(a);
+      else if (b0 == 16) k_feat_q_band<16><<<g, 256, 0, s>>>(a);
+      else if (b0 == 32) k_feat_q_band<32><<<g, 256, 0, s>>>(a);
+      else k_feat_q_band<64><<<g, 256, 0, s>>>(a);
+    } else {
+      k_feat_q<<<grid_for(npx, 256, 148 * 16), 256, 0, s>>>(a);
+    }
     k_feat_f1<<<grid_for(a.K, 256), 256, 0, s>>>(a);
     k_feat_adj<<<grid_for(nb, 256, 148 * 16), 256, 0, s>>>(a);
     k_feat_classify<<<grid_for(a.K, 256), 256, 0, s>>>(a);

@@ -186,6 +186,20 @@ def make_params(p, batch=1) -> rapid_params:
     return o
 
 
+def load_feature_model(path):
+    """SURVEY f2 model file -> rapid_params.feat_w_q16: a JSON object {"bias": b, "w": [w1, w2,
+    w3, w4]} of the linear h_theta of Eq. 6 over the features of P:271 (absolute / comparative
+    brightness, intra- / extra-region dissimilarity, each in [0, 1] or [-1, 1]), rounded to
+    Q16.16.  (Training the model is out of scope: it needs the paper's data.)"""
+    import json
+    with open(path) as f:
+        m = json.load(f)
+    w = [m["bias"]] + list(m["w"])
+    if len(w) != 5:
+        raise ValueError("a feature model has a bias and 4 weights")
+    return [int(round(float(v) * 65536)) for v in w]
+
+
 # ---- same-name wrappers of the C entry points (pointers as ints) ------------------------
 def rapid_init(device, max_pixels_total, max_superpixels_total):
     h = ctypes.c_void_p()

@@ -66,6 +66,10 @@ extern "C" {
 /* stats_mode */
 #define RAPID_STATS_REUSE 0   /* RAPID: coarsest-level sums reused (Eq. 8, exact here) */
 #define RAPID_STATS_RECOUNT 1 /* multi-scale CTFTPS: recount at every stage (checked equal) */
+#define RAPID_STATS_PYRAMID 2 /* literal image pyramid — block colour data are area x
+                                 the rounded box mean of the next finer level, S_1 from
+                                 the coarsest level, reused by Eq. 8 (the paper's approximation;
+                                 A32) */
 
 /* how the prediction step (RAPID l.3-4, Eq. 6) computes y of each superpixel */
 #define RAPID_Y_PROTO 0    /* distance of the mean colour to the prototypes (A21) */

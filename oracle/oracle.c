@@ -645,9 +645,52 @@ static int build_stage(seg_t *g, int s) {
   return 0;
 }
 
+/* f3 / A32, literal image pyramid (Eq. 8 reuse with the paper's approximation): a block's
+ * level value is the rounded (half up) area-weighted mean of its children's level values in
+ * the next finer stage, the finest stage's blocks averaging their pixels (pixels are the
+ * level of b = 1); its colour data are area x value per channel; area and position sums stay
+ * exact (full-resolution coordinates make Eq. 8's position map the identity). */
+static int build_pyramid_literal(seg_t *g) {
+  const orc_params *p = g->p;
+  for (int s = p->n_stages - 1; s >= 0; s--) {
+    stage_t *st = &g->st[s];
+    if (p->block_size[s] == 1) continue;
+    free(st->bd);
+    st->bd = (int64_t *)malloc(sizeof(int64_t) * 6 * (size_t)st->nbx * st->nby);
+    if (!st->bd) return ORC_E_OOM;
+    const stage_t *fn = (s + 1 < p->n_stages && p->block_size[s + 1] > 1) ? &g->st[s + 1] : NULL;
+    for (int j = 0; j < st->nby; j++)
+      for (int i = 0; i < st->nbx; i++) {
+        int64_t *d = st->bd + ((size_t)j * st->nbx + i) * 6;
+        const int x0 = st->xs[i], x1 = st->xs[i + 1], y0 = st->ys[j], y1 = st->ys[j + 1];
+        int64_t pix[6];
+        block_direct(g, x0, x1, y0, y1, pix); /* exact area and positions */
+        int64_t cs[3] = {pix[1], pix[2], pix[3]};
+        if (fn) { /* children: the finer stage's blocks inside this one */
+          cs[0] = cs[1] = cs[2] = 0;
+          for (int cj = 0; cj < fn->nby; cj++) {
+            if (fn->ys[cj] < y0 || fn->ys[cj] >= y1) continue;
+            for (int ci = 0; ci < fn->nbx; ci++) {
+              if (fn->xs[ci] < x0 || fn->xs[ci] >= x1) continue;
+              const int64_t *cd = fn->bd + ((size_t)cj * fn->nbx + ci) * 6;
+              cs[0] += cd[1]; cs[1] += cd[2]; cs[2] += cd[3];
+            }
+          }
+        }
+        const int64_t area = pix[0];
+        d[0] = area;
+        for (int ch = 0; ch < 3; ch++) d[1 + ch] = area * ((2 * cs[ch] + area) / (2 * area));
+        d[4] = pix[4];
+        d[5] = pix[5];
+      }
+  }
+  return 0;
+}
+
 static int build_block_sums(seg_t *g, int s) { /* O3, direct summation (b > 1 only) */
   stage_t *st = &g->st[s];
   if (g->p->block_size[s] == 1) return 0;
+  if (g->p->stats_mode == ORC_STATS_PYRAMID) return st->bd ? 0 : ORC_E_ARG; /* built up front */
   st->bd = (int64_t *)malloc(sizeof(int64_t) * 6 * (size_t)st->nbx * st->nby);
   if (!st->bd) return ORC_E_OOM;
   for (int j = 0; j < st->nby; j++)
@@ -741,6 +784,22 @@ static int seg_image(seg_t *g, int32_t *labels_out, orc_sp *sp_out) {
   free(colcell);
   free(rowcell);
 
+  if (p->stats_mode == ORC_STATS_PYRAMID) {
+    int rc2 = build_pyramid_literal(g);
+    if (rc2) return rc2;
+    /* f3: S_1 from the coarsest level's data ("average information of each superpixel at the
+     * first image level"), not from the pixels */
+    const stage_t *st = &g->st[0];
+    if (p->block_size[0] > 1) {
+      memset(g->S, 0, sizeof(int64_t) * 6 * (size_t)M);
+      for (int j = 0; j < st->nby; j++)
+        for (int i = 0; i < st->nbx; i++) {
+          const int64_t *d = st->bd + ((size_t)j * st->nbx + i) * 6;
+          int64_t *sk = g->S + (size_t)g->L[(size_t)j * st->nbx + i] * 6;
+          for (int f = 0; f < 6; f++) sk[f] += d[f];
+        }
+    }
+  }
   prop_t *props = NULL;
   int result = 0;
   for (int s = 0; s < p->n_stages; s++) {
@@ -766,7 +825,7 @@ static int seg_image(seg_t *g, int32_t *labels_out, orc_sp *sp_out) {
           NL[(size_t)j * st->nbx + i] = g->L[(size_t)pj[j] * pv->nbx + pi[i]];
       free(pi); free(pj); free(g->L);
       g->L = NL;
-      free(pv->bd); pv->bd = NULL;
+      if (p->stats_mode != ORC_STATS_PYRAMID) { free(pv->bd); pv->bd = NULL; }
     }
     g->cur = s;
     result = build_block_sums(g, s);

@@ -24,7 +24,7 @@
 
 enum { ORC_SIZE_NONE = 0, ORC_SIZE_HARD = 1, ORC_SIZE_MERGE = 2 };
 enum { ORC_MASK_OFF = 0, ORC_MASK_CLASS = 1, ORC_MASK_BSP = 2, ORC_MASK_EQ7 = 3 };
-enum { ORC_STATS_REUSE = 0, ORC_STATS_RECOUNT = 1 };
+enum { ORC_STATS_REUSE = 0, ORC_STATS_RECOUNT = 1, ORC_STATS_PYRAMID = 2 };
 /* per-phase counters */
 enum { ORC_C_CAND = 0,     /* gated boundary blocks of the phase colour */
        ORC_C_TOPO = 1,     /* ... that passed the simple-point test */

@@ -287,7 +287,7 @@ int validate(rapid_ctx *c, int H, int W, const rapid_params *p) {
     if (p->feat_w_q16[k] <= -(1ll << 31) || p->feat_w_q16[k] >= (1ll << 31))
       return fail(c, RAPID_E_RANGE, "feature weights out of (-2^31, 2^31)");
   if (p->tau2 < 0 || p->tau2 >= (1ll << 40)) return fail(c, RAPID_E_RANGE, "tau2 out of [0, 2^40)");
-  if (p->stats_mode > 1) return fail(c, RAPID_E_ARG, "stats_mode");
+  if (p->stats_mode > RAPID_STATS_PYRAMID) return fail(c, RAPID_E_ARG, "stats_mode");
   const uint64_t px = (uint64_t)p->batch * H * W;
   if (px > c->cap_px) return fail(c, RAPID_E_CAPACITY, "B*H*W exceeds max_pixels_total");
   if (px >= (1ull << 32)) return fail(c, RAPID_E_RANGE, "B*H*W must be < 2^32");
@@ -519,15 +519,16 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       if (P.st[st].b > 1) leaf = st;
     if (leaf >= 0) {
       int top = leaf;  // coarsest level written by the leaf kernel
+      const bool literal = p->stats_mode == RAPID_STATS_PYRAMID;
       if (leaf >= 1 && launch_pyramid_leaf24(sd[leaf], sd[leaf - 1], image, H, W, B,
                                              (uint64_t *)c->bsum.p + P.st[leaf].bsum_off,
-                                             (uint64_t *)c->bsum.p + P.st[leaf - 1].bsum_off, s))
+                                             (uint64_t *)c->bsum.p + P.st[leaf - 1].bsum_off, literal, s))
         top = leaf - 1;
       else
-        launch_pyramid_leaf(sd[leaf], image, H, W, B, (uint64_t *)c->bsum.p + P.st[leaf].bsum_off, s);
+        launch_pyramid_leaf(sd[leaf], image, H, W, B, (uint64_t *)c->bsum.p + P.st[leaf].bsum_off, literal, s);
       c->launches++;
       for (int st = top - 1; st >= 0; st--) {
-        launch_pyramid_up(sd[st], sd[st + 1], B, (uint64_t *)c->bsum.p + P.st[st].bsum_off, s);
+        launch_pyramid_up(sd[st], sd[st + 1], B, (uint64_t *)c->bsum.p + P.st[st].bsum_off, literal, s);
         c->launches++;
       }
     }

@@ -41,8 +41,20 @@ __global__ void k_init_sp(const InitArgs a) {
 }
 
 // K1: packed colour sums of the finest block stage, by direct summation over each block.
+// f3 / A32 literal image pyramid: a block's colour data become area x the rounded (half up)
+// mean of its exact (leaf) or level-synthesised (parent) sums, per packed channel
+__device__ __forceinline__ uint64_t lit_round(uint64_t pk, uint64_t area) {
+  uint64_t o = 0;
+#pragma unroll
+  for (int ch = 0; ch < 3; ch++) {
+    const uint64_t sc = (pk >> (21 * ch)) & 0x1FFFFFull;
+    o |= (area * ((2 * sc + area) / (2 * area))) << (21 * ch);
+  }
+  return o;
+}
+
 __global__ void k_pyramid_leaf(const StageDev st, const uint8_t *__restrict__ image, int H, int W,
-                               int B, uint64_t *__restrict__ bsum) {
+                               int B, uint64_t *__restrict__ bsum, bool literal) {
   const size_t nper = (size_t)st.nbx * st.nby;
   const size_t n = nper * B;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
@@ -60,7 +72,8 @@ __global__ void k_pyramid_leaf(const StageDev st, const uint8_t *__restrict__ im
         sb += row[3 * x + 2];
       }
     }
-    bsum[t] = (uint64_t)sr | ((uint64_t)sg << 21) | ((uint64_t)sb << 42);
+    const uint64_t pk = (uint64_t)sr | ((uint64_t)sg << 21) | ((uint64_t)sb << 42);
+    bsum[t] = literal ? lit_round(pk, (uint64_t)(x1 - x0) * (uint64_t)(y1 - y0)) : pk;
   }
 }
 
@@ -72,7 +85,7 @@ __device__ __forceinline__ uint32_t byte_of(const uint2 (&v)[3], int i) {
   return (w >> (8 * (i & 3))) & 0xffu;
 }
 __global__ void k_pyramid_leaf2(const StageDev st, const uint8_t *__restrict__ image, int H, int W,
-                                int B, uint64_t *__restrict__ bsum) {
+                                int B, uint64_t *__restrict__ bsum, bool literal) {
   const int q = st.nbx / 4;  // thread groups per block row
   const size_t n = (size_t)q * st.nby * B;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
@@ -94,6 +107,7 @@ __global__ void k_pyramid_leaf2(const StageDev st, const uint8_t *__restrict__ i
         s[ch] = byte_of(a, 6 * j + ch) + byte_of(a, 6 * j + 3 + ch) + byte_of(b, 6 * j + ch) +
                 byte_of(b, 6 * j + 3 + ch);
       out[j] = (uint64_t)s[0] | ((uint64_t)s[1] << 21) | ((uint64_t)s[2] << 42);
+      if (literal) out[j] = lit_round(out[j], 4);
     }
     uint64_t *dst = bsum + row * st.nbx + gx;
     reinterpret_cast<ulonglong2 *>(dst)[0] = make_ulonglong2(out[0], out[1]);
@@ -106,7 +120,8 @@ __global__ void k_pyramid_leaf2(const StageDev st, const uint8_t *__restrict__ i
 // 8 x 4 pixel patch (four 2x2 blocks in each of two block rows) with 8-B loads and writes the
 // eight b = 2 sums and the two b = 4 sums: the b = 4 level is not re-read from HBM.
 __global__ void k_pyramid_leaf24(const StageDev st, const StageDev up, const uint8_t *__restrict__ image, int H,
-                                 int W, int B, uint64_t *__restrict__ bsum, uint64_t *__restrict__ bsum_up) {
+                                 int W, int B, uint64_t *__restrict__ bsum, uint64_t *__restrict__ bsum_up,
+                                 bool literal) {
   const int q = st.nbx / 4;        // thread groups per block-row pair
   const int npair = st.nby / 2;    // block-row pairs per image
   const size_t n = (size_t)q * npair * B;
@@ -136,6 +151,7 @@ __global__ void k_pyramid_leaf24(const StageDev st, const StageDev up, const uin
           sc[ch] = byte_of(a, 6 * j + ch) + byte_of(a, 6 * j + 3 + ch) + byte_of(b, 6 * j + ch) +
                    byte_of(b, 6 * j + 3 + ch);
         o2[h][j] = (uint64_t)sc[0] | ((uint64_t)sc[1] << 21) | ((uint64_t)sc[2] << 42);
+        if (literal) o2[h][j] = lit_round(o2[h][j], 4);
       }
     }
     // stores: every store instruction of the warp writes whole 32-B sectors (a half-sector
@@ -165,14 +181,19 @@ __global__ void k_pyramid_leaf24(const StageDev st, const StageDev up, const uin
       }
     }
     if (valid) {  // packed fields never carry: each stays < 2^21 up to b = 90
-      const uint64_t u0 = o2[0][0] + o2[0][1] + o2[1][0] + o2[1][1], u1 = o2[0][2] + o2[0][3] + o2[1][2] + o2[1][3];
+      uint64_t u0 = o2[0][0] + o2[0][1] + o2[1][0] + o2[1][1], u1 = o2[0][2] + o2[0][3] + o2[1][2] + o2[1][3];
+      if (literal) {
+        u0 = lit_round(u0, 16);
+        u1 = lit_round(u1, 16);
+      }
       uint64_t *dup = bsum_up + ((size_t)img * up.nby + (gy >> 1)) * up.nbx + (gx >> 1);
       *reinterpret_cast<ulonglong2 *>(dup) = make_ulonglong2(u0, u1);
     }
   }
 }
 
-__global__ void k_pyramid_up(const StageDev st, const StageDev ch, int B, uint64_t *__restrict__ bsum) {
+__global__ void k_pyramid_up(const StageDev st, const StageDev ch, int B, uint64_t *__restrict__ bsum,
+                             bool literal) {
   const size_t nper = (size_t)st.nbx * st.nby;
   const size_t n = nper * B;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n;
@@ -184,6 +205,8 @@ __global__ void k_pyramid_up(const StageDev st, const StageDev ch, int B, uint64
     for (int cy = st.cys[gy]; cy < st.cys[gy + 1]; cy++)
       for (int cx = st.cxs[gx]; cx < st.cxs[gx + 1]; cx++)
         acc += ch.bsum[((size_t)img * ch.nby + cy) * ch.nbx + cx];
+    if (literal)
+      acc = lit_round(acc, (uint64_t)(st.xs[gx + 1] - st.xs[gx]) * (uint64_t)(st.ys[gy + 1] - st.ys[gy]));
     bsum[t] = acc;
   }
 }
@@ -1182,28 +1205,28 @@ void launch_init_sp(const InitArgs &a, cudaStream_t s) {
 }
 
 bool launch_pyramid_leaf24(const StageDev &st, const StageDev &up, const uint8_t *image, int H, int W, int B,
-                           uint64_t *bsum, uint64_t *bsum_up, cudaStream_t s) {
+                           uint64_t *bsum, uint64_t *bsum_up, bool literal, cudaStream_t s) {
   if (!(st.uniform && up.uniform && st.b == 2 && up.b == 4 && W % 8 == 0 && H % 4 == 0 &&
         ((uintptr_t)image & 7u) == 0))
     return false;
   const size_t n = (size_t)(st.nbx / 4) * (st.nby / 2) * B;
-  k_pyramid_leaf24<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(st, up, image, H, W, B, bsum, bsum_up);
+  k_pyramid_leaf24<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(st, up, image, H, W, B, bsum, bsum_up, literal);
   return true;
 }
 
 void launch_pyramid_leaf(const StageDev &st, const uint8_t *image, int H, int W, int B,
-                         uint64_t *bsum, cudaStream_t s) {
+                         uint64_t *bsum, bool literal, cudaStream_t s) {
   const size_t n = (size_t)st.nbx * st.nby * B;
   if (st.uniform && st.b == 2 && W % 8 == 0 && ((uintptr_t)image & 7u) == 0)
-    k_pyramid_leaf2<<<grid_for(n / 4, 256, 148 * 32), 256, 0, s>>>(st, image, H, W, B, bsum);
+    k_pyramid_leaf2<<<grid_for(n / 4, 256, 148 * 32), 256, 0, s>>>(st, image, H, W, B, bsum, literal);
   else
-    k_pyramid_leaf<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(st, image, H, W, B, bsum);
+    k_pyramid_leaf<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(st, image, H, W, B, bsum, literal);
 }
 
-void launch_pyramid_up(const StageDev &parent, const StageDev &child, int B, uint64_t *bsum,
+void launch_pyramid_up(const StageDev &parent, const StageDev &child, int B, uint64_t *bsum, bool literal,
                        cudaStream_t s) {
   const size_t n = (size_t)parent.nbx * parent.nby * B;
-  k_pyramid_up<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(parent, child, B, bsum);
+  k_pyramid_up<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(parent, child, B, bsum, literal);
 }
 
 void launch_init_map0(const InitArgs &a, cudaStream_t s) {

@@ -186,13 +186,14 @@ struct QualityArgs {
 
 // launch wrappers (all enqueue on `s`)
 void launch_init_sp(const InitArgs &a, cudaStream_t s);
+// literal: f3 literal image pyramid (A32): colour data = area x rounded level mean
 void launch_pyramid_leaf(const StageDev &st, const uint8_t *image, int H, int W, int B,
-                         uint64_t *bsum, cudaStream_t s);
-void launch_pyramid_up(const StageDev &parent, const StageDev &child, int B, uint64_t *bsum,
+                         uint64_t *bsum, bool literal, cudaStream_t s);
+void launch_pyramid_up(const StageDev &parent, const StageDev &child, int B, uint64_t *bsum, bool literal,
                        cudaStream_t s);
 // b = 2 leaf fused with its b = 4 parent (uniform dyadic stages); false when not applicable
 bool launch_pyramid_leaf24(const StageDev &st, const StageDev &up, const uint8_t *image, int H, int W, int B,
-                           uint64_t *bsum, uint64_t *bsum_up, cudaStream_t s);
+                           uint64_t *bsum, uint64_t *bsum_up, bool literal, cudaStream_t s);
 void launch_init_map0(const InitArgs &a, cudaStream_t s);
 void launch_stats0(const InitArgs &a, cudaStream_t s);
 void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s);

@@ -80,7 +80,7 @@ def hash3(seed, stream, index):
 # the oracle has its own struct with the same field meanings.
 SIZE_NONE, SIZE_HARD, SIZE_MERGE = 0, 1, 2
 MASK_OFF, MASK_CLASS, MASK_BSP, MASK_EQ7 = 0, 1, 2, 3
-STATS_REUSE, STATS_RECOUNT = 0, 1
+STATS_REUSE, STATS_RECOUNT, STATS_PYRAMID = 0, 1, 2
 Y_PROTO, Y_FEATURES = 0, 1
 # SURVEY f2 default linear model (training is out of scope; a hand-set model file): tissue
 # (pink / purple) is darker than the white background, y = +1 iff 0.85 - f1 >= 0, i.e. mean
@@ -212,12 +212,13 @@ def scaled(k: int, H: int, W: int, B: int = 1, seed_offset: int = 0) -> Workload
 
 # the paper's comparison settings on this path (Table 1).  They
 # only configure the existing kernels (run_ctftps / run_multiscale / run_rapid).
-SETTINGS = ("rapid", "ctftps", "multiscale", "rapid_features")
+SETTINGS = ("rapid", "ctftps", "multiscale", "rapid_features", "rapid_pyramid")
 
 
 def with_setting(w: Workload, setting: str) -> Workload:
     """Copy of workload `w` under one of SETTINGS: RAPID = the config's own parameters;
     rapid_features = RAPID with the f2 feature-model prediction (FEAT_W_TISSUE);
+    rapid_pyramid = RAPID on the f3 literal image pyramid (STATS_PYRAMID);
     CTFTPS = HARD size bound, no mask, REUSE; multi-scale CTFTPS = the same with statistics
     recounted at every stage (RECOUNT)."""
     import copy
@@ -227,6 +228,10 @@ def with_setting(w: Workload, setting: str) -> Workload:
     if setting == "rapid":  # the config's own parameters (configs 3-5: MERGE + CLASS + REUSE)
         return w2
     p = w2.params
+    if setting == "rapid_pyramid":  # f3: RAPID on a literal image pyramid (approximate Eq. 8)
+        p.size_mode, p.mask_rule, p.stats_mode = SIZE_MERGE, MASK_CLASS, STATS_PYRAMID
+        w2.name = f"{w.name}_{setting}"
+        return w2
     if setting == "rapid_features":  # f2: the prediction by the feature model (tissue model)
         p.size_mode, p.mask_rule, p.stats_mode = SIZE_MERGE, MASK_CLASS, STATS_REUSE
         p.y_model, p.feat_w_q16 = Y_FEATURES, list(FEAT_W_TISSUE)

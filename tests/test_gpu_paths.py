@@ -184,3 +184,26 @@ def test_feature_model_prediction_oracle_exact(cfg, side, mask):
     alive = ref.sp["alive"] == 1
     assert np.array_equal(sp["active"][alive], ref.sp["active"][alive])
     assert np.array_equal(lab, ref.labels)
+
+
+@pytest.mark.parametrize("cfg,side", [(1, 0), (2, 0), (3, 512), (5, 0)])
+def test_literal_pyramid_mode_oracle_exact(cfg, side):
+    """f3 (Eq. 8 with the paper's approximation; A32): block colour data from rounded
+    box-mean levels, S_1 from the coarsest level — bit-exact with the oracle (labels, sums,
+    counters), including the non-dyadic geometry of config 1."""
+    w = synth.scaled(cfg, side, side) if side else synth.config(cfg)
+    if cfg == 5:
+        w.seeds, w.regions, w.nuclei, w.B = w.seeds[:3], w.regions[:3], w.nuclei[:3], 3
+    p = copy.deepcopy(w.params)
+    p.stats_mode = synth.STATS_PYRAMID
+    img = w.images()
+    ref = oracle.segment(img, p)
+    r = make_ctx({}, w.pixels, w.B * p.n_superpixels)
+    try:
+        lab, sp, info = gpu_run(r, img, p)
+    finally:
+        r.close()
+    assert np.array_equal(lab, ref.labels)
+    for f in ("n", "sum_r", "sum_g", "sum_b", "sum_x", "sum_y"):
+        assert np.array_equal(sp[f], ref.sp[f]), f
+    assert np.array_equal(info.counters()[..., oracle.C_COMMIT], ref.counters[..., oracle.C_COMMIT])

@@ -19,7 +19,7 @@ ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--steps", type=int, default=5)
 a = ap.parse_args()
 rows = []
-for setting in ("rapid", "rapid_features", "ctftps", "multiscale"):
+for setting in ("rapid", "rapid_pyramid", "rapid_features", "ctftps", "multiscale"):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", str(a.config), "--steps",
                           str(a.steps), "--warmup", "3", "--no-e2e", "--no-cpu", "--setting", setting],
                          capture_output=True, text=True, check=True).stdout

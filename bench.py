@@ -95,7 +95,8 @@ def config_dict(w, extra=None):
          "block_sizes": p.block_sizes, "sweeps": p.sweeps,
          "size_mode": ["NONE", "HARD", "MERGE"][p.size_mode],
          "mask_rule": ["OFF", "CLASS", "BSP", "EQ7"][p.mask_rule],
-         "stats_mode": ["REUSE", "RECOUNT"][p.stats_mode],
+         "stats_mode": ["REUSE", "RECOUNT", "PYRAMID"][p.stats_mode],
+        "y_model": ["PROTO", "FEATURES"][getattr(p, "y_model", 0)],
          "l2": "inputs larger than L2 (image %.2f GB, labels %.2f GB); no flush" % (
              w.pixels * 3 / 1e9, w.pixels * 4 / 1e9)}
     if extra:

@@ -119,9 +119,9 @@ __global__ void k_pyramid_leaf2(const StageDev st, const uint8_t *__restrict__ i
 // Fused leaf for dyadic pyramids (b = 2 leaf, b = 4 parent, both uniform): one thread reads a
 // 8 x 4 pixel patch (four 2x2 blocks in each of two block rows) with 8-B loads and writes the
 // eight b = 2 sums and the two b = 4 sums: the b = 4 level is not re-read from HBM.
+template <bool literal>
 __global__ void k_pyramid_leaf24(const StageDev st, const StageDev up, const uint8_t *__restrict__ image, int H,
-                                 int W, int B, uint64_t *__restrict__ bsum, uint64_t *__restrict__ bsum_up,
-                                 bool literal) {
+                                 int W, int B, uint64_t *__restrict__ bsum, uint64_t *__restrict__ bsum_up) {
   const int q = st.nbx / 4;        // thread groups per block-row pair
   const int npair = st.nby / 2;    // block-row pairs per image
   const size_t n = (size_t)q * npair * B;
@@ -1210,7 +1210,8 @@ bool launch_pyramid_leaf24(const StageDev &st, const StageDev &up, const uint8_t
         ((uintptr_t)image & 7u) == 0))
     return false;
   const size_t n = (size_t)(st.nbx / 4) * (st.nby / 2) * B;
-  k_pyramid_leaf24<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(st, up, image, H, W, B, bsum, bsum_up, literal);
+  if (literal) k_pyramid_leaf24<true><<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(st, up, image, H, W, B, bsum, bsum_up);
+  else k_pyramid_leaf24<false><<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(st, up, image, H, W, B, bsum, bsum_up);
   return true;
 }
 

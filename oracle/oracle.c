@@ -169,7 +169,14 @@ static void snapshot(seg_t *g) { /* O5 */
     const int64_t *s = g->S + (size_t)k * 6;
     g->nsnap[k] = s[0];
     if (!g->alive[k] || s[0] <= 0) continue;
-    for (int ch = 0; ch < 3; ch++) orc_round_mean(s[1 + ch], s[0], &g->cq[(size_t)k * 3 + ch]);
+    /* A33: a colour sum outside [0, 255 n] (possible only with the literal pyramid's
+     * synthesised data, f3) gives a mean clamped to the intensity range */
+    for (int ch = 0; ch < 3; ch++) {
+      int64_t *q = &g->cq[(size_t)k * 3 + ch];
+      if (s[1 + ch] < 0) *q = 0;
+      else if (s[1 + ch] > 255 * s[0]) *q = (int64_t)255 << FRAC;
+      else orc_round_mean(s[1 + ch], s[0], q);
+    }
     for (int d = 0; d < 2; d++) orc_round_mean(s[4 + d], s[0], &g->mq[(size_t)k * 2 + d]);
   }
 }
@@ -532,7 +539,9 @@ static void predict_features(seg_t *g) {
   const size_t nb = (size_t)st->nbx * st->nby;
   uint64_t *pairs = (uint64_t *)malloc(sizeof(uint64_t) * (4 * nb + 1));  /* directed adjacent pairs */
   size_t np = 0;
-  /* Q by the pixels of every block of the current map */
+  /* S and Q by the pixels of every block of the current map (the features read the image:
+   * with the literal pyramid, f3, the superpixel sums are approximations) */
+  int64_t *Sp = (int64_t *)calloc((size_t)M, sizeof(int64_t));
   for (int j = 0; j < st->nby; j++)
     for (int i = 0; i < st->nbx; i++) {
       const int32_t a = lab(g, i, j);
@@ -540,21 +549,19 @@ static void predict_features(seg_t *g) {
         for (int x = st->xs[i]; x < st->xs[i + 1]; x++) {
           const uint8_t *px = g->I + ((size_t)y * g->W + x) * 3;
           const int64_t s = (int64_t)px[0] + px[1] + px[2];
+          Sp[a] += s;
           Q[a] += (i128)(s * s);
         }
     }
   i128 Simg = 0, Nimg = 0;
   for (int k = 0; k < M; k++)
     if (g->alive[k]) {
-      Simg += (i128)(g->S[(size_t)k * 6 + 1] + g->S[(size_t)k * 6 + 2] + g->S[(size_t)k * 6 + 3]);
+      Simg += (i128)Sp[k];
       Nimg += (i128)g->S[(size_t)k * 6];
     }
   const int64_t fimg = rhu(Simg << 16, 765 * Nimg);
   for (int k = 0; k < M; k++)
-    if (g->alive[k]) {
-      const i128 n = g->S[(size_t)k * 6], S = g->S[(size_t)k * 6 + 1] + g->S[(size_t)k * 6 + 2] + g->S[(size_t)k * 6 + 3];
-      f1[k] = rhu(S << 16, 765 * n);
-    }
+    if (g->alive[k]) f1[k] = rhu((i128)Sp[k] << 16, 765 * (i128)g->S[(size_t)k * 6]);
   for (int j = 0; j < st->nby; j++)
     for (int i = 0; i < st->nbx; i++) {
       const int32_t a = lab(g, i, j);
@@ -574,7 +581,7 @@ static void predict_features(seg_t *g) {
   }
   for (int k = 0; k < M; k++) {
     if (!g->alive[k]) { g->y[k] = 0; continue; }
-    const i128 n = g->S[(size_t)k * 6], S = g->S[(size_t)k * 6 + 1] + g->S[(size_t)k * 6 + 2] + g->S[(size_t)k * 6 + 3];
+    const i128 n = g->S[(size_t)k * 6], S = Sp[k];
     const int64_t f2 = f1[k] - fimg;
     const int64_t f3 = rhu((n * Q[k] - S * S) << 16, 585225 * n * n);
     const int64_t f4 = deg[k] ? rhu(dsum[k], deg[k]) : 0;
@@ -582,7 +589,7 @@ static void predict_features(seg_t *g) {
                    (i128)p->feat_w_q16[3] * f3 + (i128)p->feat_w_q16[4] * f4;
     g->y[k] = h >= 0 ? 1 : -1;
   }
-  free(Q); free(f1); free(dsum); free(deg); free(pairs);
+  free(Q); free(f1); free(dsum); free(deg); free(pairs); free(Sp);
 }
 
 static void predict(seg_t *g) {

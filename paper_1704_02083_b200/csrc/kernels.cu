@@ -271,9 +271,16 @@ __device__ __forceinline__ void make_rec(const SpDev &sp, int k) {
       if (r >= (long long)twon) q++;
       return (unsigned long long)q;
     };
-    c0 = (uint32_t)qdiv((s[1] << (FRAC + 1)) + n);
-    c1 = (uint32_t)qdiv((s[2] << (FRAC + 1)) + n);
-    c2 = (uint32_t)qdiv((s[3] << (FRAC + 1)) + n);
+    // A33: a colour sum outside [0, 255 n] (only the literal pyramid's synthesised data makes
+    // one, f3) gives a mean clamped to the intensity range
+    auto cmean = [&](unsigned long long sc) -> uint32_t {
+      if ((long long)sc < 0) return 0u;
+      if (sc > 255ull * n) return 255u << FRAC;
+      return (uint32_t)qdiv((sc << (FRAC + 1)) + n);
+    };
+    c0 = cmean(s[1]);
+    c1 = cmean(s[2]);
+    c2 = cmean(s[3]);
     mx = (int32_t)qdiv((s[4] << (FRAC + 1)) + n);
     my = (int32_t)qdiv((s[5] << (FRAC + 1)) + n);
   }
@@ -722,13 +729,14 @@ __device__ __forceinline__ int resolve(const SpDev &sp, int kb, int l, bool rema
 // ---------------------------------------------------- f2: feature model of the prediction
 // A31 (oracle.h / oracle.c predict_features): brightness (r+g+b)/3; per superpixel n,
 // S = sum(r+g+b), Q = sum((r+g+b)^2) over its pixels at stage 0 (after the stage-0 merges).
-// scratch[k*SUMW + 0] = Q, + 2 = f1, + 3 = sum |f1 - f1_q|, + 4 = distinct neighbours, + 5 = f3;
+// scratch[k*SUMW + 0] = Q, + 1 = S (from the pixels: with the literal pyramid the superpixel
+// sums are approximations, A33), + 2 = f1, + 3 = sum |f1 - f1_q|, + 4 = distinct neighbours, + 5 = f3;
 // image totals S, N at scratch[img*M*SUMW + 6 / 7].  Everything exact (integers, round half up).
 __device__ __forceinline__ long long rhu128(__int128 num, __int128 den) {
   return (long long)((2 * num + den) / (2 * den));
 }
 
-__global__ void k_feat_q(const PredictArgs a) {  // Q per superpixel from the pixels
+__global__ void k_feat_q(const PredictArgs a) {  // S, Q per superpixel from the pixels
   const bool rm = *a.remap_pending != 0u;
   const StageDev &st = a.st;
   const size_t nper = (size_t)a.H * a.W, n = nper * a.B;
@@ -737,7 +745,7 @@ __global__ void k_feat_q(const PredictArgs a) {  // Q per superpixel from the pi
     const size_t t = base + threadIdx.x;
     const bool valid = t < n;
     int key = 0;
-    unsigned long long v = 0;
+    unsigned long long v = 0, w = 0;
     if (valid) {
       const int img = (int)(t / nper);
       const size_t r = t - (size_t)img * nper;
@@ -748,15 +756,22 @@ __global__ void k_feat_q(const PredictArgs a) {  // Q per superpixel from the pi
       const uint8_t *p = a.image + t * 3;
       const unsigned long long s = (unsigned long long)p[0] + p[1] + p[2];
       v = s * s;
+      w = s;
     }
     const WarpRun run = warp_runs(valid, key);
     const int lane = lane_id();
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long u = __shfl_up_sync(FULL, v, o);
-      if (lane - o >= run.start) v += u;
+      const unsigned long long u = __shfl_up_sync(FULL, v, o), uw = __shfl_up_sync(FULL, w, o);
+      if (lane - o >= run.start) {
+        v += u;
+        w += uw;
+      }
     }
-    if (valid && run.end) atomicAdd(&a.scratch[(size_t)key * SUMW + 0], v);
+    if (valid && run.end) {
+      atomicAdd(&a.scratch[(size_t)key * SUMW + 0], v);
+      atomicAdd(&a.scratch[(size_t)key * SUMW + 1], w);
+    }
   }
 }
 
@@ -766,7 +781,7 @@ __global__ void k_feat_q(const PredictArgs a) {  // Q per superpixel from the pi
 // shared memory; one atomic per block and band.
 template <int b0>
 __global__ void __launch_bounds__(256) k_feat_q_band(const PredictArgs a) {
-  __shared__ unsigned long long s_q[32];  // blocks of the band (256 / b0 <= 32)
+  __shared__ unsigned long long s_q[32], s_s[32];  // blocks of the band (256 / b0 <= 32)
   const bool rm = *a.remap_pending != 0u;
   const StageDev &st = a.st;
   const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -777,13 +792,13 @@ __global__ void __launch_bounds__(256) k_feat_q_band(const PredictArgs a) {
   for (unsigned band = blockIdx.x; band < nbands; band += gridDim.x) {
     const unsigned gx = band % gcols, r2 = band / gcols;
     const int by = (int)(r2 % bands_y), img = (int)(r2 / bands_y);
-    if (threadIdx.x < 32) s_q[threadIdx.x] = 0ull;
+    if (threadIdx.x < 32) s_q[threadIdx.x] = s_s[threadIdx.x] = 0ull;
     __syncthreads();
     const int x0 = (int)gx * 256 + 8 * lane;
 #pragma unroll
     for (int row = warp; row < b0; row += 8) {  // b0 / 8 independent rows per warp
       const int y = by * b0 + row;
-      unsigned long long q = 0;
+      unsigned long long q = 0, sv = 0;
       if (x0 < a.W) {
         const uint2 *p = reinterpret_cast<const uint2 *>(a.image + (((size_t)img * a.H + y) * a.W + x0) * 3);
         const uint2 v[3] = {__ldcs(p), __ldcs(p + 1), __ldcs(p + 2)};
@@ -791,10 +806,17 @@ __global__ void __launch_bounds__(256) k_feat_q_band(const PredictArgs a) {
         for (int j = 0; j < 8; j++) {
           const unsigned long long t = (unsigned long long)byte_of(v, 3 * j) + byte_of(v, 3 * j + 1) + byte_of(v, 3 * j + 2);
           q += t * t;
+          sv += t;
         }
       }
-      for (int o = 1; o < per; o <<= 1) q += __shfl_xor_sync(FULL, q, o);
-      if ((lane % per) == 0 && x0 < a.W) atomicAdd(&s_q[lane / per], q);
+      for (int o = 1; o < per; o <<= 1) {
+        q += __shfl_xor_sync(FULL, q, o);
+        sv += __shfl_xor_sync(FULL, sv, o);
+      }
+      if ((lane % per) == 0 && x0 < a.W) {
+        atomicAdd(&s_q[lane / per], q);
+        atomicAdd(&s_s[lane / per], sv);
+      }
     }
     __syncthreads();
     if (threadIdx.x < nblk) {
@@ -803,6 +825,7 @@ __global__ void __launch_bounds__(256) k_feat_q_band(const PredictArgs a) {
         const int kb = img * a.M;
         const int l = resolve(a.sp, kb, st.map[((size_t)img * st.nby + by) * st.nbx + bx], rm);
         atomicAdd(&a.scratch[(size_t)(kb + l) * SUMW + 0], s_q[threadIdx.x]);
+        atomicAdd(&a.scratch[(size_t)(kb + l) * SUMW + 1], s_s[threadIdx.x]);
       }
     }
     __syncthreads();
@@ -818,7 +841,7 @@ __global__ void k_feat_f1(const PredictArgs a) {  // f1, f3 per superpixel; imag
     if (valid) {
       const unsigned long long *sm = a.sp.sums + (size_t)k * SUMW;
       n = (long long)sm[0];
-      S = (long long)(sm[1] + sm[2] + sm[3]);
+      S = (long long)a.scratch[(size_t)k * SUMW + 1];
       const unsigned long long Q = a.scratch[(size_t)k * SUMW + 0];
       // f1: S 2^16 < 2^58 and 765 n < 2^42 fit 64 bits
       const long long f1 = (long long)((2ull * ((unsigned long long)S << 16) + 765ull * n) / (2ull * 765ull * n));

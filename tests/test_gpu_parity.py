@@ -179,3 +179,38 @@ def test_debug_stop_points_match_oracle(rapid):
         g = rapid.debug_map(cap)
         rapid.debug_stop(0)
         assert np.array_equal(g, o.map), pt
+
+
+# ----------------------------------------------------------------------- randomized sweep
+def test_random_all_options_combined(rapid):
+    """Random small cases over every option at once (size mode, mask rule, y model, stats
+    mode, lambdas, stage lists, final grain, batches), each bit-exact with the oracle."""
+    import os
+    rng = np.random.default_rng(int(os.environ.get("RAPID_RANDOM_SEED", "2024")))
+    for case in range(int(os.environ.get("RAPID_RANDOM_CASES", "24"))):
+        B = int(rng.integers(1, 4))
+        H, W = int(rng.integers(24, 140)), int(rng.integers(24, 140))
+        imgs = np.stack([synth.image(H, W, int(rng.integers(1 << 30)), int(rng.integers(2, 12)),
+                                     int(rng.integers(0, 40)), int(rng.integers(0, 600))) for _ in range(B)])
+        while True:  # a superpixel count whose grid fits the image
+            M = int(rng.integers(1, max(2, H * W // 60)))
+            try:
+                oracle.grid(H, W, M)
+                break
+            except oracle.OracleError:
+                pass
+        top = int(rng.choice([8, 16, 32]))
+        sizes = [top >> k for k in range(int(np.log2(top)) + 1)]
+        if rng.random() < 0.3:
+            sizes = sizes[:-2]  # final grain 4
+        mask = int(rng.integers(0, 4))
+        p = P(M, sizes, int(rng.integers(1, 5)), int(rng.integers(0, 4 * 65536)), int(rng.integers(0, 64 * 65536)),
+              size_mode=int(rng.integers(0, 3)), mask=mask, tau2=int(rng.integers(200, 6000)),
+              stats=int(rng.choice([0, 1, 2])))
+        if mask and rng.random() < 0.5:
+            p.y_model = synth.Y_FEATURES
+            p.feat_w_q16 = [int(v) for v in rng.integers(-70000, 70000, 5)]
+        try:
+            assert_parity(rapid, imgs, p)
+        except AssertionError as e:
+            raise AssertionError(f"case {case}: B={B} H={H} W={W} params={p}: {e}") from None

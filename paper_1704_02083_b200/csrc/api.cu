@@ -98,6 +98,7 @@ struct rapid_ctx {
   DevBuf himg, hlab;
   // occupancy
   int scan_grid = 0, eval_grid = 0, sweep_grid = 0, tiles_grid = 0;  // persistent grid sizes (CTAs)
+  int sweep_gpw = 2;  // K4 word groups per warp (RAPID_SWEEP_GPW overrides, A/B testing)
   bool use_bset = true;  // RAPID_SWEEP=scan selects the full-scan path K4a + K4b (A/B testing)
   // CUDA graph of the whole segmentation (one launch per call): captured on a private stream,
   // replayed while the key (buffers, geometry, params, profiling level, plan) is unchanged
@@ -634,13 +635,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           pa.gating = gating;
           pa.bset = c->use_bset ? (uint32_t *)c->bset.p : nullptr;
           pa.wq = &ctl->wq[g];
-          {  // enough warp iterations to occupy every sweep warp twice (tile count upper bound)
-            const size_t words = (size_t)sd[st].tiles_x * sd[st].tiles_y * B * (TY / 2);
-            const size_t warps = (size_t)c->sweep_grid * 8;
-            int G = 32;
-            while (G > 4 && words / G < 2 * warps) G >>= 1;
-            pa.gwords = G;
-          }
+          pa.gpw = c->sweep_gpw;
           pa.size_mode = (int)p->size_mode;
           pa.l_num = p->l_num; pa.l_den = p->l_den;
           pa.lam_pos = p->lambda_pos_q16;
@@ -876,6 +871,7 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   c->scan_grid = c->sm_count * scan_occupancy();
   c->eval_grid = c->sm_count * eval_occupancy();
   c->sweep_grid = c->sm_count * sweep_occupancy();
+  if (const char *e = getenv("RAPID_SWEEP_GPW")) c->sweep_gpw = std::max(1, atoi(e));
   c->tiles_grid = c->sm_count * tiles_occupancy();
   {
     const char *e = getenv("RAPID_SWEEP");

@@ -26,7 +26,7 @@ struct PhaseArgs {
   const unsigned long long *prev; // counters of the previous sweep (phase 0), or null
   uint32_t *victim_any;
   uint32_t *bset;            // boundary sets of the stage (null: full-scan path K4a/K4b)
-  int32_t gwords;            // k_sweep: bset words per warp iteration (4..32)
+  int32_t gpw;               // k_sweep: word groups per warp to aim for (sizes the groups)
   unsigned int *wq;          // k_sweep: work-queue counter of this phase (zeroed per call)
 };
 

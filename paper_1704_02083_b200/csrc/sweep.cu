@@ -711,9 +711,13 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
   const StageDev &st = a.st;
   const int nbx = st.nbx, nby = st.nby;
   const unsigned ntiles = a.worklist ? *a.nwork : (unsigned)(st.tiles_x * st.tiles_y) * (unsigned)a.B;
-  const unsigned G = (unsigned)a.gwords;  // words per warp iteration (4..32, power of 2)
+  const unsigned nw = (gridDim.x * blockDim.x) >> 5;
+  // words per warp iteration (4..32, power of 2): the largest giving every warp gpw groups of
+  // the (device-side) worklist; larger groups fill the rounds better and take fewer of the
+  // queue's same-address atomics (measured: gpw 2 best at config 4)
+  unsigned G = 32;
+  while (G > 4 && ntiles * (TY / 2) / G < (unsigned)a.gpw * nw) G >>= 1;
   const unsigned ngroups = (ntiles * (TY / 2) + G - 1) / G;
-  const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
   const int colour = a.cx | (a.cy << 1);
   __shared__ unsigned s_cnt[5];  // cand, topo, prop, srej, commit (per CTA; flushed at the end)
   __shared__ uint32_t s_simple[8];  // 256-bit truth table of simple_point (E_topo) by ring mask
@@ -726,8 +730,6 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
   __syncthreads();
   unsigned long long pbase = 0;  // this warp's reserved proposal slots
   int pleft = 0;
-  (void)gw;
-  (void)nw;
   // dynamic distribution of the word groups (one returned atomic per group and warp): the
   // per-group work varies with the boundary density, static striding left a 10 % tail
   for (unsigned g = 0;;) {

@@ -806,54 +806,55 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
         const int nq[4] = {nq0, nq1, nq2, nq3};
         const bool bnd = (nq0 >= 0 && nq0 != A) | (nq1 >= 0 && nq1 != A) | (nq2 >= 0 && nq2 != A) |
                          (nq3 >= 0 && nq3 != A);
-        bool keep = bnd;
-        Rec recA;
-        if (bnd) {
-          recA = a.sp.rec[kb + A];
-          if (a.gating == 1) keep = ((recA.cq2f >> 16) & F_ACTIVE) != 0u;
+        // topology (E_topo) and the distinct candidate labels need only the window; the
+        // records of A and of the candidates are then loaded together (one dependent L2
+        // round trip instead of two)
+        const unsigned m8 = (unsigned)(nq0 == A) | ((unsigned)(dNE == A) << 1) | ((unsigned)(nq1 == A) << 2) |
+                            ((unsigned)(dSE == A) << 3) | ((unsigned)(nq2 == A) << 4) |
+                            ((unsigned)(dSW == A) << 5) | ((unsigned)(nq3 == A) << 6) |
+                            ((unsigned)(dNW == A) << 7);
+        const bool topo_ok = (s_simple[m8 >> 5] >> (m8 & 31u)) & 1u;
+        // distinct candidate labels (A8), compacted: cb[0..nb) with the slot mask cm of each;
+        // maskA = slots labelled A.  Records: first 16 B (means + flags).
+        int cb[4] = {0, 0, 0, 0};
+        unsigned cm[4] = {0u, 0u, 0u, 0u};
+        unsigned maskA = 0;
+        int nb = 0;
+#pragma unroll
+        for (int s = 0; s < 4; s++) {
+          const int L = nq[s];
+          if (L == A) maskA |= 1u << s;
+          if (L < 0 || L == A) continue;
+          bool found = false;
+#pragma unroll
+          for (int r = 0; r < s; r++)
+            if (r < nb && cb[r] == L) {
+              cm[r] |= 1u << s;
+              found = true;
+            }
+          if (!found) {
+#pragma unroll
+            for (int r = 0; r <= s; r++)
+              if (r == nb) {
+                cb[r] = L;
+                cm[r] = 1u << s;
+              }
+            nb++;
+          }
         }
+        Rec recA;
+        int4 rn[4];
+        const bool need_rn = bnd && (topo_ok || a.gating == 2);
+        if (bnd) recA = a.sp.rec[kb + A];
+#pragma unroll
+        for (int k2 = 0; k2 < 4; k2++)
+          rn[k2] = (need_rn && k2 < nb) ? __ldg(reinterpret_cast<const int4 *>(&a.sp.rec[kb + cb[k2]]))
+                                        : make_int4(0, 0, 0, 0);
+        bool keep = bnd;
+        if (bnd && a.gating == 1) keep = ((recA.cq2f >> 16) & F_ACTIVE) != 0u;
         if (!keep) {
           atomicAnd(&a.bset[xj], ~(1u << bit));  // stale: no longer a gated boundary block
         } else {
-          const unsigned m8 = (unsigned)(nq0 == A) | ((unsigned)(dNE == A) << 1) | ((unsigned)(nq1 == A) << 2) |
-                              ((unsigned)(dSE == A) << 3) | ((unsigned)(nq2 == A) << 4) |
-                              ((unsigned)(dSW == A) << 5) | ((unsigned)(nq3 == A) << 6) |
-                              ((unsigned)(dNW == A) << 7);
-          const bool topo_ok = (s_simple[m8 >> 5] >> (m8 & 31u)) & 1u;
-          // distinct candidate labels (A8), compacted: cb[0..nb) with the slot mask cm of each;
-          // maskA = slots labelled A.  Records: first 16 B (means + flags).
-          int cb[4] = {0, 0, 0, 0};
-          unsigned cm[4] = {0u, 0u, 0u, 0u};
-          unsigned maskA = 0;
-          int nb = 0;
-#pragma unroll
-          for (int s = 0; s < 4; s++) {
-            const int L = nq[s];
-            if (L == A) maskA |= 1u << s;
-            if (L < 0 || L == A) continue;
-            bool found = false;
-#pragma unroll
-            for (int r = 0; r < s; r++)
-              if (r < nb && cb[r] == L) {
-                cm[r] |= 1u << s;
-                found = true;
-              }
-            if (!found) {
-#pragma unroll
-              for (int r = 0; r <= s; r++)
-                if (r == nb) {
-                  cb[r] = L;
-                  cm[r] = 1u << s;
-                }
-              nb++;
-            }
-          }
-          int4 rn[4];
-          const bool need_rn = topo_ok || a.gating == 2;
-#pragma unroll
-          for (int k2 = 0; k2 < 4; k2++)
-            rn[k2] = (need_rn && k2 < nb) ? __ldg(reinterpret_cast<const int4 *>(&a.sp.rec[kb + cb[k2]]))
-                                          : make_int4(0, 0, 0, 0);
           cand = true;
           if (a.gating == 2) {  // Eq. 7: a neighbour of another label and another class
             const unsigned yA = (recA.cq2f >> 18) & 3u;

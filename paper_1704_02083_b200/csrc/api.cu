@@ -410,6 +410,8 @@ StageDev stage_dev(rapid_ctx *c, int s, int32_t *labels_out) {
   for (size_t j = 0; j < S.ys.size() && d.uniform; j++) d.uniform = S.ys[j] == (int32_t)(j * S.b);
   d.fd_tx = make_fastdiv((uint32_t)S.tiles_x);
   d.fd_ty = make_fastdiv((uint32_t)S.tiles_y);
+  d.fd_nbx = make_fastdivu((uint32_t)S.nbx);
+  d.fd_nper = make_fastdivu((uint32_t)((size_t)S.nbx * S.nby));
   d.xs = T + S.o_xs;
   d.ys = T + S.o_ys;
   d.px = T + S.o_px;

@@ -49,12 +49,27 @@ inline FastDiv make_fastdiv(uint32_t d) {
 __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
   return f.d <= 1 ? n : (__umulhi(n, f.m) >> f.s);
 }
+// Division of any n < 2^32 by d in [1, 2^32): with M = ceil(2^64 / d) (d >= 2),
+// floor(n/d) = umul64hi(n, M), since n (M - 2^64/d) / 2^64 < 2^-32 <= 1/d.
+struct FastDivU {
+  unsigned long long M;
+  uint32_t d;
+};
+inline FastDivU make_fastdivu(uint32_t d) {
+  FastDivU f{0ull, d};
+  if (d >= 2) f.M = ~0ull / d + 1ull;
+  return f;
+}
+__device__ __forceinline__ uint32_t fdivu(uint32_t n, const FastDivU &f) {
+  return f.d <= 1 ? n : (uint32_t)__umul64hi((unsigned long long)n, f.M);
+}
 
 struct StageDev {
   int32_t nbx, nby, b;
   int32_t uniform;               // 1: every block is b x b with xs[i] = i*b, ys[j] = j*b
   int32_t tiles_x, tiles_y;      // sweep tiles per image
   FastDiv fd_tx, fd_ty;          // division by tiles_x / tiles_y
+  FastDivU fd_nbx, fd_nper;      // division by nbx / nbx * nby (block index -> img, gy, gx)
   const int32_t *xs, *ys;        // block boundaries (nbx+1, nby+1)
   const int32_t *px, *py;        // parent block index in stage s-1 (s > 0)
   const int32_t *cxs, *cys;      // first child index in stage s+1 (nbx+1, nby+1)

@@ -979,7 +979,6 @@ template <bool PIXEL>
 __global__ void __launch_bounds__(256) k_commit(const PhaseArgs a) {
   const unsigned long long n = cta_count(a.prev, a.prop_count);
   if (n == 0) return;
-  const size_t nper = (size_t)a.st.nbx * a.st.nby;
   unsigned c_commit = 0, c_rej = 0;
   for (unsigned long long base = blockIdx.x * 256ull; base < n; base += gridDim.x * 256ull) {
     const unsigned long long i = base + threadIdx.x;
@@ -992,24 +991,26 @@ __global__ void __launch_bounds__(256) k_commit(const PhaseArgs a) {
       const size_t idx = pr.x;
       A = (int)pr.y;
       B = (int)pr.z;
-      const int img = (int)(idx / nper);
-      const size_t r = idx - (size_t)img * nper;
-      const int gy = (int)(r / a.st.nbx), gx = (int)(r - (size_t)gy * a.st.nbx);
+      const int img = (int)fdivu(pr.x, a.st.fd_nper);
+      const uint32_t r = pr.x - (uint32_t)img * a.st.fd_nper.d;
+      const int gy = (int)fdivu(r, a.st.fd_nbx), gx = (int)(r - (uint32_t)gy * (uint32_t)a.st.nbx);
       kb = img * a.M;
+      // the block's data (loads at block stages) is issued with the record and outflow loads
+      if (PIXEL) {
+        d[0] = 1; d[1] = pr.w & 0xffu; d[2] = (pr.w >> 8) & 0xffu; d[3] = (pr.w >> 16) & 0xffu;
+        d[4] = gx; d[5] = gy;
+      } else {
+        block_data_blk(a.st, img, gx, gy, d);
+      }
       const Rec ra = a.sp.rec[kb + A];
       // O6' all-or-nothing budget: the total proposed outflow must keep A >= l * InitSize (A19)
       ok = !(((long long)ra.n - (long long)a.sp.out[kb + A]) * a.l_den < a.l_num * (long long)ra.init);
       if (ok) {
-        if (PIXEL) {
-          d[0] = 1; d[1] = pr.w & 0xffu; d[2] = (pr.w >> 8) & 0xffu; d[3] = (pr.w >> 16) & 0xffu;
-          d[4] = gx; d[5] = gy;
-        } else {
-          block_data_blk(a.st, img, gx, gy, d);
-        }
         a.st.map[idx] = B;
         if (a.bset) bset_insert(a.bset, a.st, img, gx, gy, pr.w >> 24);
       } else {
         rej = true;
+        for (int f = 0; f < 6; f++) d[f] = 0;
         if (a.size_mode == 2) {
           a.sp.victim[kb + A] = 1;
           *a.victim_any = 1u;

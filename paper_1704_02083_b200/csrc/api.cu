@@ -99,6 +99,7 @@ struct rapid_ctx {
   // occupancy
   int scan_grid = 0, eval_grid = 0, sweep_grid = 0, tiles_grid = 0;  // persistent grid sizes (CTAs)
   int sweep_gpw = 2;  // K4 word groups per warp (RAPID_SWEEP_GPW overrides, A/B testing)
+  bool fuse_bset = false;  // RAPID_FUSE_BSET=1: dyadic transitions also write the next stage's boundary sets (measured: no faster than the separate pass)
   bool use_bset = true;  // RAPID_SWEEP=scan selects the full-scan path K4a + K4b (A/B testing)
   // CUDA graph of the whole segmentation (one launch per call): captured on a private stream,
   // replayed while the key (buffers, geometry, params, profiling level, plan) is unchanged
@@ -568,6 +569,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
   for (int st = 0; st < nst; st++) {
     const bool pixel = P.st[st].b == 1;
     const bool use_work = st > 0 && tile_gate;
+    const int gating = (st > 0 && mask != RAPID_MASK_OFF) ? (mask == RAPID_MASK_EQ7 ? 2 : 1) : 0;
+    bool bset_done = false;
     if (st > 0) {
       Timer tm(c, s, RAPID_K_TRANSITION, st);
       TransArgs ta;
@@ -579,7 +582,9 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       ta.gate = use_work ? 1 : 0;
       ta.worklist = (int32_t *)c->work.p;
       ta.nwork = &ctl->nwork[st];
-      launch_transition(ta, s);
+      ta.bset = (c->use_bset && c->fuse_bset) ? (uint32_t *)c->bset.p : nullptr;
+      ta.gating = gating;
+      bset_done = launch_transition(ta, s);
       c->launches++;
       if (p->stats_mode == RAPID_STATS_RECOUNT) {
         RecountArgs ra;
@@ -592,8 +597,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
         launch_recount(ra, pixel, grid_k, s, &c->launches);
       }
     }
-    const int gating = (st > 0 && mask != RAPID_MASK_OFF) ? (mask == RAPID_MASK_EQ7 ? 2 : 1) : 0;
-    if (c->use_bset) {  // boundary sets of the stage (maintained by the commits from here on)
+    if (c->use_bset && !bset_done) {  // boundary sets of the stage (maintained by the commits from here on)
       Timer tm(c, s, RAPID_K_TRANSITION, st);
       PhaseArgs ba{};
       ba.st = sd[st];
@@ -874,6 +878,7 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   c->eval_grid = c->sm_count * eval_occupancy();
   c->sweep_grid = c->sm_count * sweep_occupancy();
   if (const char *e = getenv("RAPID_SWEEP_GPW")) c->sweep_gpw = std::max(1, atoi(e));
+  if (const char *e = getenv("RAPID_FUSE_BSET")) c->fuse_bset = e[0] == '1';
   c->tiles_grid = c->sm_count * tiles_occupancy();
   {
     const char *e = getenv("RAPID_SWEEP");

@@ -1025,58 +1025,122 @@ __global__ void __launch_bounds__(256) k_transition(const TransArgs a) {
   }
 }
 
-// Dyadic fast path (both stages uniform, b_prev = 2 b_next): the parent of child (x, y) is
-// (x >> 1, y >> 1), so a parent row yields two identical child rows.  Persistent CTAs of 128
-// threads, one tile per iteration; a thread writes 4 children x 2 rows from 2 parent labels.
+// Dyadic fast path (both stages uniform, b_prev = 2 b_next, so nx.nbx = 2 pv.nbx): the parent
+// of child (x, y) is (x >> 1, y >> 1), so a parent row yields two identical child rows.
+// Persistent CTAs of 128 threads, one 64 x 16-child tile (32 x 8 parents) per iteration; thread
+// (r, q) = (u >> 4, u & 15) writes children 4q..4q+3 of rows 2r, 2r+1 from parents 2q, 2q+1 of
+// parent row r.  The next tile's parents are loaded while this one is written (two loads in
+// flight per thread).  BSET: the boundary sets of the next stage come from the parents too (a
+// child's outer neighbours are its parent's neighbours, its siblings share its label): the
+// remapped parents plus a one-parent halo go through shared memory, each thread forms its 8
+// children's bits (boundary and static gate) and half-warps OR them into the tile's 32 words —
+// the next stage's bset build pass (a full read of the new map) is not needed.
+template <bool BSET>
 __global__ void __launch_bounds__(128) k_transition_dyadic(const TransArgs a) {
+  __shared__ int32_t s_lab[10][34];  // parent rows -1..8, columns -1..32 of the tile (remapped)
   const StageDev &pv = a.prev, &nx = a.next;
   const unsigned ntiles = (unsigned)(nx.tiles_x * nx.tiles_y) * (unsigned)a.B;
   const bool rm = *a.remap_pending != 0u;
-  const bool vec = (nx.nbx & 3) == 0 && (pv.nbx & 1) == 0;
-  const int u = threadIdx.x;
-  for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  const bool vec = (pv.nbx & 1) == 0;
+  const int u = threadIdx.x, q = u & 15, r = u >> 4;
+  auto load_par = [&](unsigned t, int &p0, int &p1) {
+    p0 = p1 = -1;
+    if (t >= ntiles) return;
     const uint32_t rr = fdiv(t, nx.fd_tx), img = fdiv(rr, nx.fd_ty);
-    const int gx = (int)(t - rr * (uint32_t)nx.tiles_x) * TX + 4 * (u & 15);
-    const int gy = (int)(rr - img * (uint32_t)nx.tiles_y) * TY + 2 * (u >> 4);
+    const int px = (int)(t - rr * (uint32_t)nx.tiles_x) * (TX / 2) + 2 * q;
+    const int py = (int)(rr - img * (uint32_t)nx.tiles_y) * (TY / 2) + r;
+    if (py >= pv.nby || px >= pv.nbx) return;
+    const int32_t *prow = pv.map + ((size_t)img * pv.nby + py) * pv.nbx;
+    if (vec) {
+      const int2 pp = *reinterpret_cast<const int2 *>(prow + px);
+      p0 = pp.x;
+      p1 = pp.y;
+    } else {
+      p0 = prow[px];
+      if (px + 1 < pv.nbx) p1 = prow[px + 1];
+    }
+  };
+  int n0, n1;
+  load_par(blockIdx.x, n0, n1);
+  for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int p0 = n0, p1 = n1;
+    load_par(t + gridDim.x, n0, n1);  // prefetch
+    const uint32_t rr = fdiv(t, nx.fd_tx), img = fdiv(rr, nx.fd_ty);
+    const int tpx = (int)(t - rr * (uint32_t)nx.tiles_x) * (TX / 2), tpy = (int)(rr - img * (uint32_t)nx.tiles_y) * (TY / 2);
     const int kb = (int)img * a.M;
-    int act = 0;
-    if (gy < nx.nby && gx < nx.nbx) {
-      const int32_t *prow = pv.map + ((size_t)img * pv.nby + (gy >> 1)) * pv.nbx;
-      const int px = gx >> 1;
-      int p0, p1 = -1;
-      if (vec) {
-        const int2 pp = *reinterpret_cast<const int2 *>(prow + px);
-        p0 = pp.x;
-        p1 = pp.y;
-      } else {
-        p0 = prow[px];
-        if (px + 1 < pv.nbx) p1 = prow[px + 1];
+    auto res = [&](int p) { return (p >= 0 && rm && !a.sp.alive[kb + p]) ? a.sp.remap[kb + p] : p; };
+    p0 = res(p0);
+    p1 = res(p1);
+    const bool need_act = a.gate || (BSET && a.gating == 1);
+    const int a0 = (p0 >= 0 && need_act) ? a.sp.active[kb + p0] : 0;
+    const int a1 = (p1 >= 0 && need_act) ? a.sp.active[kb + p1] : 0;
+    if (BSET) {  // remapped parents and halo into shared memory
+      s_lab[r + 1][1 + 2 * q] = p0;
+      s_lab[r + 1][2 + 2 * q] = p1;
+      if (u < 80) {
+        int hy, hx;
+        if (u < 32) { hy = -1; hx = u; }
+        else if (u < 64) { hy = 8; hx = u - 32; }
+        else if (u < 72) { hy = u - 64; hx = -1; }
+        else { hy = u - 72; hx = 32; }
+        const int y = tpy + hy, x = tpx + hx;
+        int v = -1;
+        if (y >= 0 && y < pv.nby && x >= 0 && x < pv.nbx) v = res(pv.map[((size_t)img * pv.nby + y) * pv.nbx + x]);
+        s_lab[hy + 1][hx + 1] = v;
       }
-      if (rm && !a.sp.alive[kb + p0]) p0 = a.sp.remap[kb + p0];
-      if (p1 >= 0 && rm && !a.sp.alive[kb + p1]) p1 = a.sp.remap[kb + p1];
-      if (a.gate) act = a.sp.active[kb + p0] | (p1 >= 0 ? a.sp.active[kb + p1] : 0);
-      int32_t *dst = nx.map + ((size_t)img * nx.nby + gy) * nx.nbx + gx;
-      const bool two = gy + 1 < nx.nby;
+    }
+    const int py = tpy + r, px = tpx + 2 * q;
+    if (py < pv.nby && px < pv.nbx) {
+      int32_t *dst = nx.map + ((size_t)img * nx.nby + 2 * py) * nx.nbx + 2 * px;
       if (vec) {
         const int4 v = make_int4(p0, p0, p1, p1);
         *reinterpret_cast<int4 *>(dst) = v;
-        if (two) *reinterpret_cast<int4 *>(dst + nx.nbx) = v;
+        *reinterpret_cast<int4 *>(dst + nx.nbx) = v;
       } else {
         const int l[4] = {p0, p0, p1, p1};
 #pragma unroll
         for (int k = 0; k < 4; k++)
-          if (gx + k < nx.nbx) {
+          if (2 * px + k < nx.nbx) {
             dst[k] = l[k];
-            if (two) dst[nx.nbx + k] = l[k];
+            dst[nx.nbx + k] = l[k];
           }
       }
     }
-    if (a.gate) {
-      act = __syncthreads_or(act);
-      if (threadIdx.x == 0 && act) {
-        const unsigned p = atomicAdd(a.nwork, 1u);
-        a.worklist[p] = (int)t;
+    if (BSET) {
+      __syncthreads();
+      // child (i, j) of this thread: parent column pc = 2q + (i >> 1); horizontal outer
+      // neighbour on side i & 1, vertical on side j; word (colour (i & 1) + 2 j, plane row r),
+      // bit 2q + (i >> 1)
+      uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int pc = 2 * q + h, L = h ? p1 : p0;
+        const bool gate = a.gating != 1 || (h ? a1 : a0);
+        if (L < 0 || !gate) continue;
+        const int lw = s_lab[r + 1][pc], le = s_lab[r + 1][pc + 2];
+        const int lu = s_lab[r][pc + 1], ld = s_lab[r + 2][pc + 1];
+        const bool bw = lw >= 0 && lw != L, be = le >= 0 && le != L;
+        const bool bu = lu >= 0 && lu != L, bd = ld >= 0 && ld != L;
+        const uint32_t bit = 1u << (2 * q + h);
+        if (bw | bu) w[0] |= bit;  // (i even, j = 0): colour 0
+        if (be | bu) w[1] |= bit;  // (i odd, j = 0): colour 1
+        if (bw | bd) w[2] |= bit;  // (i even, j = 1): colour 2
+        if (be | bd) w[3] |= bit;  // (i odd, j = 1): colour 3
       }
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1)
+#pragma unroll
+        for (int c = 0; c < 4; c++) w[c] |= __shfl_xor_sync(0xffffffffu, w[c], o);
+      if (q == 0) {
+        uint32_t *tw = a.bset + (size_t)t * 32 + r;
+#pragma unroll
+        for (int c = 0; c < 4; c++) tw[c * (TY / 2)] = w[c];
+      }
+    }
+    const int act = __syncthreads_or(a.gate ? (a0 | a1) : 0);
+    if (a.gate && threadIdx.x == 0 && act) {
+      const unsigned p = atomicAdd(a.nwork, 1u);
+      a.worklist[p] = (int)t;
     }
   }
 }
@@ -1340,16 +1404,19 @@ void launch_predict(const PredictArgs &a, int grid, cudaStream_t s, int *nlaunch
   *nlaunch += 3;
 }
 
-void launch_transition(const TransArgs &a, cudaStream_t s) {
+bool launch_transition(const TransArgs &a, cudaStream_t s) {
   const unsigned ntiles = (unsigned)(a.next.tiles_x * a.next.tiles_y) * (unsigned)a.B;
   if (a.prev.uniform && a.next.uniform && a.prev.b == 2 * a.next.b) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    k_transition_dyadic<<<std::min<unsigned>(ntiles, (unsigned)sms * 16), 128, 0, s>>>(a);
-  } else {
-    k_transition<<<ntiles, 256, 0, s>>>(a);
+    const unsigned grid = std::min<unsigned>(ntiles, (unsigned)sms * 16);
+    if (a.bset) k_transition_dyadic<true><<<grid, 128, 0, s>>>(a);
+    else k_transition_dyadic<false><<<grid, 128, 0, s>>>(a);
+    return a.bset != nullptr;
   }
+  k_transition<<<ntiles, 256, 0, s>>>(a);
+  return false;
 }
 
 void launch_recount(const RecountArgs &a, bool pixel, int grid, cudaStream_t s, int *nlaunch) {

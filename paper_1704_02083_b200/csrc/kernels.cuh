@@ -140,6 +140,8 @@ struct TransArgs {
   int32_t gate;              // 1: build the active-tile worklist of `next`
   int32_t *worklist;
   unsigned int *nwork;
+  uint32_t *bset;            // dyadic path: also write the boundary sets of `next` (else null)
+  int32_t gating;            // static gate of the boundary sets (as PhaseArgs::gating)
 };
 
 struct InitArgs {
@@ -217,7 +219,8 @@ bool launch_merge_adjacency_tma(const MergeArgs &a, const void *tmap, int grid, 
 int tiles_occupancy();
 void launch_quality(const QualityArgs &a, int sms, cudaStream_t s);
 void launch_predict(const PredictArgs &a, int grid, cudaStream_t s, int *nlaunch);
-void launch_transition(const TransArgs &a, cudaStream_t s);
+// returns true when it also wrote the boundary sets of `next` (dyadic path with a.bset)
+bool launch_transition(const TransArgs &a, cudaStream_t s);
 void launch_recount(const RecountArgs &a, bool pixel, int grid, cudaStream_t s, int *nlaunch);
 void launch_final(const FinalArgs &a, bool upsample, cudaStream_t s);
 void launch_count_window(const StageDev &st, const SpDev &sp, int B, int M, unsigned long long *out,

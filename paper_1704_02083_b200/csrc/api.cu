@@ -99,6 +99,7 @@ struct rapid_ctx {
   // occupancy
   int scan_grid = 0, eval_grid = 0, sweep_grid = 0, tiles_grid = 0;  // persistent grid sizes (CTAs)
   int sweep_gpw = 2;  // K4 word groups per warp (RAPID_SWEEP_GPW overrides, A/B testing)
+  bool fuse_snap = false;  // RAPID_FUSE_SNAP=1: K3 of the next phase runs at the end of a cooperative K5 (measured: same step time)
   bool fuse_bset = false;  // RAPID_FUSE_BSET=1: dyadic transitions also write the next stage's boundary sets (measured: no faster than the separate pass)
   bool use_bset = true;  // RAPID_SWEEP=scan selects the full-scan path K4a + K4b (A/B testing)
   // CUDA graph of the whole segmentation (one launch per call): captured on a private stream,
@@ -483,6 +484,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
   const int B = P.B, M = P.M, nst = P.nst, K = B * M;
   const int sweeps = (int)p->sweeps;
   const int gated_sz = p->size_mode != RAPID_SIZE_NONE;
+  const bool fused_snap = gated_sz && c->fuse_snap;  // K3 folded into the previous K5
   const int grid_k = c->sm_count * 4;
   Ctl *ctl = c->ctl;
   c->launches = 0;
@@ -625,7 +627,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       }
       for (int t = 0; t < sweeps; t++) {
         for (int ph = 0; ph < 4; ph++, g++) {
-          if (!(t == 0 && ph == 0)) {
+          if (!(t == 0 && ph == 0) && !fused_snap) {  // (fused: the previous commit refreshed them)
             Timer t2(c, s, RAPID_K_SNAPSHOT, st);
             SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1)};
             launch_snapshot(sa, grid_k, s);
@@ -675,7 +677,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           }
           if (gated_sz) {
             Timer t2(c, s, RAPID_K_COMMIT, st);
-            launch_commit(pa, pixel, c->sm_count * 8, s);  // latency-bound gathers: full occupancy
+            if (fused_snap) launch_commit_snap(pa, pixel, c->sm_count, s);
+            else launch_commit(pa, pixel, c->sm_count * 8, s);  // latency-bound gathers: full occupancy
             c->launches++;
           }
           if (stop_at(RAPID_STOP_PHASE, st, t, ph)) return RAPID_OK;
@@ -684,7 +687,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     }
     {  // snapshot of the last phase's changes (merge round / prediction read it)
       Timer t2(c, s, RAPID_K_SNAPSHOT, st);
-      if (g > 0) {
+      if (g > 0 && !fused_snap) {
         SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1)};
         launch_snapshot(sa, grid_k, s);
         c->launches++;
@@ -879,6 +882,7 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   c->sweep_grid = c->sm_count * sweep_occupancy();
   if (const char *e = getenv("RAPID_SWEEP_GPW")) c->sweep_gpw = std::max(1, atoi(e));
   if (const char *e = getenv("RAPID_FUSE_BSET")) c->fuse_bset = e[0] == '1';
+  if (const char *e = getenv("RAPID_FUSE_SNAP")) c->fuse_snap = e[0] == '1';
   c->tiles_grid = c->sm_count * tiles_occupancy();
   {
     const char *e = getenv("RAPID_SWEEP");

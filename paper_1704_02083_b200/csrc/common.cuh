@@ -212,10 +212,22 @@ __device__ __forceinline__ void agg_sums_small(bool valid, int key, const long l
          ((unsigned long long)d[3] << 46);
     u1 = (unsigned long long)d[4] | ((unsigned long long)d[5] << 26);
   }
-  // group the lanes by key (not only adjacent runs): the group's lowest lane gathers the
-  // others' words with shuffles (iterations = largest group - 1) and issues the atomics
-  const unsigned grp = __match_any_sync(FULL, valid ? key : -1 - lane);
-  const bool leader = valid && (__ffs(grp) - 1) == lane;
+  // runs of adjacent lanes with equal keys (the usual case: a warp's moves come from a few
+  // boundary stretches) are summed by a segmented scan; the run ends holding the totals are
+  // then grouped by key (runs of one key that are not adjacent) and the group's lowest run end
+  // gathers the others' words with shuffles (iterations = largest group - 1, usually 0)
+  const WarpRun run = warp_runs(valid, key);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t0 = __shfl_up_sync(FULL, u0, o), t1 = __shfl_up_sync(FULL, u1, o);
+    if (lane - o >= run.start) {
+      u0 += t0;
+      u1 += t1;
+    }
+  }
+  const bool rend = valid && run.end;
+  const unsigned grp = __match_any_sync(FULL, rend ? key : -1 - lane);
+  const bool leader = rend && (__ffs(grp) - 1) == lane;
   unsigned rem = leader ? grp & ~(1u << lane) : 0u;
   const unsigned long long v0 = u0, v1 = u1;
   while (__any_sync(FULL, rem != 0u)) {

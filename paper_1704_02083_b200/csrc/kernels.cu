@@ -248,97 +248,8 @@ __global__ void k_stats0(const InitArgs a) {
 }
 
 // ------------------------------------------------------------------ K3: snapshot
-__device__ __forceinline__ void make_rec(const SpDev &sp, int k) {
-  const unsigned long long *s = sp.sums + (size_t)k * SUMW;
-  const unsigned long long n = s[0];
-  Rec r;
-  r.n = (int32_t)n;
-  r.init = sp.init[k];
-  const uint32_t flags = (uint32_t)sp.alive[k] | ((uint32_t)sp.active[k] << 1) |
-                         ((uint32_t)(sp.y[k] + 1) << 2);
-  uint32_t c0 = 0, c1 = 0, c2 = 0;
-  int32_t mx = 0, my = 0;
-  if (n > 0) {
-    const unsigned long long twon = 2 * n;
-    // round-half-up(2^F S / n) = floor((2^(F+1) S + n) / 2n)  (A24).  Exact quotient from a
-    // double reciprocal estimate (relative error < 2^-50, quotients < 2^25, so the estimate is
-    // within one of the quotient) and one integer correction step each way.
-    const double rcp = 1.0 / (double)twon;
-    auto qdiv = [&](unsigned long long num) -> unsigned long long {
-      long long q = (long long)((double)num * rcp);
-      long long r = (long long)(num - (unsigned long long)q * twon);
-      if (r < 0) { q--; r += (long long)twon; }
-      if (r >= (long long)twon) q++;
-      return (unsigned long long)q;
-    };
-    // A33: a colour sum outside [0, 255 n] (only the literal pyramid's synthesised data makes
-    // one, f3) gives a mean clamped to the intensity range
-    auto cmean = [&](unsigned long long sc) -> uint32_t {
-      if ((long long)sc < 0) return 0u;
-      if (sc > 255ull * n) return 255u << FRAC;
-      return (uint32_t)qdiv((sc << (FRAC + 1)) + n);
-    };
-    c0 = cmean(s[1]);
-    c1 = cmean(s[2]);
-    c2 = cmean(s[3]);
-    mx = (int32_t)qdiv((s[4] << (FRAC + 1)) + n);
-    my = (int32_t)qdiv((s[5] << (FRAC + 1)) + n);
-  }
-  r.mux = mx;
-  r.muy = my;
-  r.cq01 = c0 | (c1 << 16);
-  r.cq2f = c2 | (flags << 16);
-  r.pad0 = r.pad1 = 0;
-  sp.rec[k] = r;
-}
-
 __global__ void k_snapshot(const SnapArgs a) {
-  // full refresh (stamp 0) or only the superpixels stamped dirty by the previous phase.  A warp
-  // takes 128 consecutive stamps (one 16-B load per lane; the array is padded to a multiple of
-  // 4), compacts the dirty ones and refreshes them 32 at a time (one record per lane).
-  const int lane = lane_id();
-  const int n4 = (a.K + 3) >> 2;
-  const int nchunks = (n4 + 31) >> 5;
-  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  for (int ch = wid; ch < nchunks; ch += nw) {
-    const int i = ch * 32 + lane;
-    unsigned m = 0;
-    if (i < n4) {
-      const uint4 s4 = a.stamp ? *reinterpret_cast<const uint4 *>(a.sp.dirty + 4 * (size_t)i) : make_uint4(0, 0, 0, 0);
-      const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
-#pragma unroll
-      for (int j = 0; j < 4; j++)
-        if (4 * i + j < a.K && (a.stamp == 0u || sv[j] == a.stamp)) m |= 1u << j;
-    }
-    unsigned incl = __popc(m);
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned v = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const unsigned total = __shfl_sync(FULL, incl, 31);
-    for (unsigned rb = 0; rb < total; rb += 32) {
-      const unsigned k = rb + lane;
-      int j = 0;  // source lane: #lanes with incl <= k
-#pragma unroll
-      for (int h = 16; h > 0; h >>= 1) {
-        const unsigned v = __shfl_sync(FULL, incl, j + h - 1);
-        if (v <= k) j += h;
-      }
-      const unsigned mj = __shfl_sync(FULL, m, j);
-      unsigned r = k - (__shfl_sync(FULL, incl, j) - __popc(mj));
-      if (k < total) {
-        int bit = 0;  // r-th set bit of the 4-bit mask
-        unsigned mm = mj;
-        while (r) {
-          mm &= mm - 1;
-          r--;
-        }
-        bit = __ffs(mm) - 1;
-        make_rec(a.sp, 4 * (ch * 32 + j) + bit);
-      }
-    }
-  }
+  snapshot_warps(a, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5);
 }
 
 

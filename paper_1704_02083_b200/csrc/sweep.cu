@@ -24,9 +24,13 @@
 #include <cudaTypedefs.h>
 #include <cstdlib>
 
+#include <algorithm>
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 
 namespace rapid {
+namespace cg = cooperative_groups;
 
 typedef __int128 i128;
 
@@ -102,13 +106,16 @@ __device__ __forceinline__ i128 delta_e(const RecV &ra, const RecV &rb, const lo
 // Work count of a list-driven kernel, read once per CTA (thread 0) and broadcast through
 // shared memory: 0 when the sweep is skipped (A25) or the list is empty, and also 0 for
 // CTAs whose first element lies beyond the list.  Must be called by all threads.
+// the phase's list length as seen by this CTA: 0 when the CTA has no entry (per_cta) — or only
+// when the list is empty (grid-uniform, for kernels with a grid barrier)
 __device__ __forceinline__ unsigned long long cta_count(const unsigned long long *prev,
-                                                         const unsigned long long *count) {
+                                                         const unsigned long long *count,
+                                                         bool per_cta = true) {
   __shared__ unsigned long long s_n;
   if (threadIdx.x == 0) s_n = sweep_skipped(prev) ? 0ull : *count;
   __syncthreads();
   const unsigned long long n = s_n;
-  return (unsigned long long)blockIdx.x * blockDim.x < n ? n : 0ull;
+  return (!per_cta || (unsigned long long)blockIdx.x * blockDim.x < n) ? n : 0ull;
 }
 
 
@@ -975,10 +982,12 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
 }
 
 // ------------------------------------------------------------------ K5: commit
-template <bool PIXEL>
+// SNAP (cooperative launch, every CTA resident): after a grid barrier the same CTAs refresh the
+// records this commit stamped dirty (K3 of the next phase / of the stage end, without a launch)
+template <bool PIXEL, bool SNAP>
 __global__ void __launch_bounds__(256) k_commit(const PhaseArgs a) {
-  const unsigned long long n = cta_count(a.prev, a.prop_count);
-  if (n == 0) return;
+  const unsigned long long n = cta_count(a.prev, a.prop_count, !SNAP);
+  if (n == 0) return;  // SNAP: grid-uniform (an empty list stamps nothing to refresh)
   unsigned c_commit = 0, c_rej = 0;
   for (unsigned long long base = blockIdx.x * 256ull; base < n; base += gridDim.x * 256ull) {
     const unsigned long long i = base + threadIdx.x;
@@ -1030,6 +1039,11 @@ __global__ void __launch_bounds__(256) k_commit(const PhaseArgs a) {
   if (lane_id() == 0) {
     if (c_commit) atomicAdd(&a.cnt[4], (unsigned long long)c_commit);
     if (c_rej) atomicAdd(&a.cnt[5], (unsigned long long)c_rej);
+  }
+  if (SNAP) {  // n is grid-uniform (cta_count per_cta = false): every CTA gets here or none did
+    cg::this_grid().sync();
+    const SnapArgs sa{a.sp, a.B * a.M, a.stamp};
+    snapshot_warps(sa, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5);
   }
 }
 
@@ -1154,8 +1168,18 @@ void launch_sweep(const PhaseArgs &a, bool pixel, int sm_count, cudaStream_t s) 
 }
 
 void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
-  if (pixel) k_commit<true><<<grid, 256, 0, s>>>(a);
-  else k_commit<false><<<grid, 256, 0, s>>>(a);
+  if (pixel) k_commit<true, false><<<grid, 256, 0, s>>>(a);
+  else k_commit<false, false><<<grid, 256, 0, s>>>(a);
+}
+
+// K5 + the next K3 in one cooperative launch (grid = every CTA that fits at once)
+void launch_commit_snap(const PhaseArgs &a, bool pixel, int sm_count, cudaStream_t s) {
+  const void *fn = pixel ? (const void *)k_commit<true, true> : (const void *)k_commit<false, true>;
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 256, 0);
+  PhaseArgs copy = a;
+  void *args[] = {&copy};
+  cudaLaunchCooperativeKernel(fn, dim3(sm_count * std::max(nb, 1)), dim3(256), args, 0, s);
 }
 
 }  // namespace rapid

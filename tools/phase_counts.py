@@ -26,8 +26,8 @@ r.segment(img, w.params)
 _, info = r.stats(0)
 ns = len(w.params.block_sizes)
 cnt = info.counters()
-print("| stage (b) | active tiles / tiles | sweep.phase: cand / topo / prop / commit |")
-print("|---|---|---|")
+print("| stage (b) | active tiles / tiles | victims / merges | sweep.phase: cand / topo / prop / commit |")
+print("|---|---|---|---|")
 for s in range(ns):
     cells = []
     for t in range(int(info.stage_sweeps_run[s])):
@@ -35,4 +35,5 @@ for s in range(ns):
             c = cnt[s, t, ph]
             cells.append(f"{t}.{ph}: {c[0]}/{c[1]}/{c[2]}/{c[4]}")
     print(f"| {s} ({w.params.block_sizes[s]}) | {info.stage_active_tiles[s]} / {info.stage_tiles[s]} | "
+          f"{info.stage_victims[s]} / {info.stage_merges[s]} | "
           + "; ".join(cells) + " |")

@@ -35,6 +35,7 @@ struct StagePlan {
   std::vector<int32_t> xs, ys, px, py, cxs, cys;
   size_t o_xs = 0, o_ys = 0, o_px = 0, o_py = 0, o_cxs = 0, o_cys = 0;
   size_t bsum_off = 0;  // in uint64 elements
+  bool smallb = false;  // block stage with (max block area) x (max coordinate) < 2^22: K4's 32-bit position factors
 };
 
 struct Plan {
@@ -324,6 +325,10 @@ int build_plan(rapid_ctx *c, int H, int W, const rapid_params *p) {
     S.nby = (int)S.ys.size() - 1;
     S.tiles_x = (S.nbx + TX - 1) / TX;
     S.tiles_y = (S.nby + TY - 1) / TY;
+    int64_t mw = 0, mh = 0;
+    for (int i = 0; i < S.nbx; i++) mw = std::max<int64_t>(mw, S.xs[i + 1] - S.xs[i]);
+    for (int j = 0; j < S.nby; j++) mh = std::max<int64_t>(mh, S.ys[j + 1] - S.ys[j]);
+    S.smallb = S.b > 1 && mw * mh * (int64_t)(std::max(H, W) - 1) < (int64_t(1) << 22);
   }
   for (int s = 0; s < nst; s++) {
     StagePlan &S = N.st[s];
@@ -661,7 +666,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           if (gated_sz) cudaMemsetAsync(c->out, 0, sizeof(int32_t) * K, s);
           if (c->use_bset) {
             Timer t2(c, s, RAPID_K_PROPOSE, st);
-            launch_sweep(pa, pixel, c->sm_count, s);
+            launch_sweep(pa, pixel, P.st[st].smallb, c->sm_count, s);
             c->launches++;
           } else {
             {

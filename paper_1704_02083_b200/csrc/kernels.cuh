@@ -300,7 +300,7 @@ void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
 void launch_commit_snap(const PhaseArgs &a, bool pixel, int sm_count, cudaStream_t s);
 // boundary-set sweep: K4 build (once per stage) and the fused bitset-driven sweep
 void launch_bset_build(const PhaseArgs &a, const void *tmap, int grid, cudaStream_t s);
-void launch_sweep(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
+void launch_sweep(const PhaseArgs &a, bool pixel, bool smallb, int sm_count, cudaStream_t s);
 int sweep_occupancy();
 int scan_occupancy();
 int eval_occupancy();

@@ -681,7 +681,7 @@ __device__ __forceinline__ i128 mul_u31_s64(long long lam, long long v) {
 // record rb: E = X * 2^16 + lam_pos * dP with X = colour part + lam_b * dB2 (exact in int64)
 // and dP the position part (exact in int64).  At the pixel stage (n = 1, values
 // < 2^8, coordinates < 2^16) every factor fits 32 bits, so each product is one IMAD.WIDE.
-template <bool PIXEL>
+template <bool PIXEL, bool SMALLB = false>
 __device__ __forceinline__ i128 energy(const Rec &ra, const int4 rb, const int d[6], long long dB2,
                                        long long lam_pos, long long lam_b) {
   const int cA0 = (int)(ra.cq01 & 0xffffu), cA1 = (int)(ra.cq01 >> 16), cA2 = (int)(ra.cq2f & 0xffffu);
@@ -701,8 +701,15 @@ __device__ __forceinline__ i128 energy(const Rec &ra, const int4 rb, const int d
     X = (long long)(cB0 - cA0) * (n * (cB0 + cA0) - (d[1] << (FRAC + 1))) +
         (long long)(cB1 - cA1) * (n * (cB1 + cA1) - (d[2] << (FRAC + 1))) +
         (long long)(cB2 - cA2) * (n * (cB2 + cA2) - (d[3] << (FRAC + 1))) + lam_b * dB2;
-    dP = (long long)(rb.x - ra.mux) * ((long long)n * ((long long)rb.x + ra.mux) - ((long long)d[4] << (FRAC + 1))) +
-         (long long)(rb.y - ra.muy) * ((long long)n * ((long long)rb.y + ra.muy) - ((long long)d[5] << (FRAC + 1)));
+    if (SMALLB) {
+      // n * max coordinate < 2^22 (checked per stage on the host): |n (mB + mA) - 2^9 sum| < 2^31,
+      // so each position product is one 32 x 32 -> 64 IMAD.WIDE as at the pixel stage
+      dP = (long long)(rb.x - ra.mux) * (n * (rb.x + ra.mux) - (d[4] << (FRAC + 1))) +
+           (long long)(rb.y - ra.muy) * (n * (rb.y + ra.muy) - (d[5] << (FRAC + 1)));
+    } else {
+      dP = (long long)(rb.x - ra.mux) * ((long long)n * ((long long)rb.x + ra.mux) - ((long long)d[4] << (FRAC + 1))) +
+           (long long)(rb.y - ra.muy) * ((long long)n * ((long long)rb.y + ra.muy) - ((long long)d[5] << (FRAC + 1)));
+    }
   }
   return ((i128)X << 16) + mul_u31_s64(lam_pos, dP);
 }
@@ -711,7 +718,7 @@ __device__ __forceinline__ i128 energy(const Rec &ra, const int4 rb, const int d
 // tiles; lane l loads bset word (tile l/8, colour c, plane row l%8), the set bits are
 // distributed 32 at a time over the lanes, and every lane re-tests its block from the label
 // map (boundary, static gate, simple point, Eq. 7), then evaluates Eqs. 1-3 as K4b does.
-template <bool PIXEL, bool GATED, int MINB>
+template <bool PIXEL, bool GATED, int MINB, bool SMALLB = false>
 __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) {
   if (sweep_skipped(a.prev)) return;
   const int lane = lane_id();
@@ -898,7 +905,7 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
             for (int k2 = 0; k2 < 4; k2++) {
               if (k2 >= nb) break;
               const int B = cb[k2];
-              const i128 E = energy<PIXEL>(recA, rn[k2], d, 2ll * (wA - wsum(cm[k2])), a.lam_pos, a.lam_b);
+              const i128 E = energy<PIXEL, SMALLB>(recA, rn[k2], d, 2ll * (wA - wsum(cm[k2])), a.lam_pos, a.lam_b);
               if (!hv || E < bestE || (E == bestE && B < bestB)) {
                 hv = true;
                 bestE = E;
@@ -1108,6 +1115,7 @@ void launch_eval(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
 // registers), the block stages at 3 (80; their 64-bit position sums spill at 64).
 // RAPID_SWEEP_MINB=2..4 forces one budget for every stage (A/B testing).
 static int g_sweep_minb = 0;
+static int g_sweep_minb_small = 3;  // RAPID_SWEEP_MINB_SMALL: CTAs/SM of the small-block variant
 
 template <int MB>
 static int sweep_occ() {
@@ -1119,6 +1127,8 @@ static int sweep_occ() {
 int sweep_occupancy() {
   const char *e = getenv("RAPID_SWEEP_MINB");
   if (e && e[0] >= '2' && e[0] <= '4') g_sweep_minb = e[0] - '0';
+  const char *es = getenv("RAPID_SWEEP_MINB_SMALL");
+  if (es && es[0] >= '2' && es[0] <= '4') g_sweep_minb_small = es[0] - '0';
   return g_sweep_minb == 2 ? sweep_occ<2>() : g_sweep_minb == 3 ? sweep_occ<3>() : sweep_occ<4>();
 }
 
@@ -1150,16 +1160,18 @@ bool launch_merge_adjacency_tma(const MergeArgs &m, const void *tmap, int grid, 
   return true;
 }
 
-void launch_sweep(const PhaseArgs &a, bool pixel, int sm_count, cudaStream_t s) {
+void launch_sweep(const PhaseArgs &a, bool pixel, bool smallb, int sm_count, cudaStream_t s) {
   const bool gated = a.size_mode != 0;
   static int occ[5] = {0, 0, 0, 0, 0};
-  const int mb = g_sweep_minb ? g_sweep_minb : (pixel ? 4 : 3);
+  const int mb = g_sweep_minb ? g_sweep_minb : (pixel ? 4 : smallb ? g_sweep_minb_small : 3);
   if (!occ[mb]) occ[mb] = mb == 2 ? sweep_occ<2>() : mb == 3 ? sweep_occ<3>() : sweep_occ<4>();
   const int grid = sm_count * occ[mb];
-#define RAPID_SWEEP_LAUNCH(MB)                                                    \
-  if (pixel && gated) k_sweep<true, true, MB><<<grid, K4B_THREADS, 0, s>>>(a);    \
-  else if (pixel) k_sweep<true, false, MB><<<grid, K4B_THREADS, 0, s>>>(a);       \
-  else if (gated) k_sweep<false, true, MB><<<grid, K4B_THREADS, 0, s>>>(a);       \
+#define RAPID_SWEEP_LAUNCH(MB)                                                         \
+  if (pixel && gated) k_sweep<true, true, MB><<<grid, K4B_THREADS, 0, s>>>(a);         \
+  else if (pixel) k_sweep<true, false, MB><<<grid, K4B_THREADS, 0, s>>>(a);            \
+  else if (gated && smallb) k_sweep<false, true, MB, true><<<grid, K4B_THREADS, 0, s>>>(a); \
+  else if (smallb) k_sweep<false, false, MB, true><<<grid, K4B_THREADS, 0, s>>>(a);    \
+  else if (gated) k_sweep<false, true, MB><<<grid, K4B_THREADS, 0, s>>>(a);            \
   else k_sweep<false, false, MB><<<grid, K4B_THREADS, 0, s>>>(a);
   if (mb == 2) { RAPID_SWEEP_LAUNCH(2) }
   else if (mb == 4) { RAPID_SWEEP_LAUNCH(4) }

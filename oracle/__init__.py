@@ -130,6 +130,8 @@ def lib():
         L.orc_yokoi_c4.restype = ctypes.c_int
         L.orc_round_mean.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
         L.orc_round_mean.restype = None
+        L.orc_colour_mean.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64)]
+        L.orc_colour_mean.restype = None
         L.orc_block_move.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.POINTER(OrcParams), ctypes.POINTER(ctypes.c_int32),
                                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_uint64)]
@@ -273,4 +275,11 @@ def block_move(win, means, d, e, params):
 def round_mean(S, n):
     q = ctypes.c_int64()
     lib().orc_round_mean(S, n, ctypes.byref(q))
+    return q.value
+
+
+def colour_mean(S, n):
+    """O5's rounding of a colour channel's mean, clamped to [0, 255] (DESIGN A33)."""
+    q = ctypes.c_int64()
+    lib().orc_colour_mean(S, n, ctypes.byref(q))
     return q.value

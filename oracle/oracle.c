@@ -90,6 +90,16 @@ int orc_yokoi_c4(int m) {
 
 /* ------------------------------------------------------------------ O5 -- */
 /* q = round-half-up(2^F * S / n) = floor((2^(F+1) S + n) / (2n)), S >= 0, n > 0 */
+/* A33 (f3): a colour channel's snapshot mean is O5's rounding of S / n clamped to the
+ * intensity range [0, 255] — a sum outside [0, 255 n] arises only from the literal pyramid's
+ * synthesised block data, where blocks leave a superpixel with finer data than they entered
+ * with; otherwise this is orc_round_mean. */
+void orc_colour_mean(int64_t S, int64_t n, int64_t *q) {
+  if (S < 0) *q = 0;
+  else if (S > 255 * n) *q = (int64_t)255 << FRAC;
+  else orc_round_mean(S, n, q);
+}
+
 void orc_round_mean(int64_t S, int64_t n, int64_t *q) {
   i128 num = ((i128)S << (FRAC + 1)) + n;
   *q = (int64_t)(num / (2 * (i128)n));
@@ -169,14 +179,7 @@ static void snapshot(seg_t *g) { /* O5 */
     const int64_t *s = g->S + (size_t)k * 6;
     g->nsnap[k] = s[0];
     if (!g->alive[k] || s[0] <= 0) continue;
-    /* A33: a colour sum outside [0, 255 n] (possible only with the literal pyramid's
-     * synthesised data, f3) gives a mean clamped to the intensity range */
-    for (int ch = 0; ch < 3; ch++) {
-      int64_t *q = &g->cq[(size_t)k * 3 + ch];
-      if (s[1 + ch] < 0) *q = 0;
-      else if (s[1 + ch] > 255 * s[0]) *q = (int64_t)255 << FRAC;
-      else orc_round_mean(s[1 + ch], s[0], q);
-    }
+    for (int ch = 0; ch < 3; ch++) orc_colour_mean(s[1 + ch], s[0], &g->cq[(size_t)k * 3 + ch]);
     for (int d = 0; d < 2; d++) orc_round_mean(s[4 + d], s[0], &g->mq[(size_t)k * 2 + d]);
   }
 }

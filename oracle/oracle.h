@@ -110,6 +110,7 @@ int orc_stage_axis(int len, int b, const int32_t *cuts, int ncuts,  /* O2 */
                    int32_t *out, int cap);
 int orc_yokoi_c4(int ring_mask);                                    /* A9 */
 void orc_round_mean(int64_t S, int64_t n, int64_t *q);              /* O5 */
+void orc_colour_mean(int64_t S, int64_t n, int64_t *q);             /* O5 + A33 clamp */
 /* O6 steps 2-6 for one block in isolation (see oracle.c) */
 int orc_block_move(const int32_t *win, const int64_t *means, const int64_t *d, const int64_t *e,
                    const orc_params *p, int32_t *B_out, int64_t *dE_hi, uint64_t *dE_lo);

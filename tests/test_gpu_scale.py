@@ -140,7 +140,8 @@ def test_config4_sampled_block_decisions_match_oracle(cfg4):
                 continue
             if l not in means_of:
                 n = int(sp["n"][l])
-                means_of[l] = [oracle.round_mean(int(sp[f][l]), n) for f in ("sum_r", "sum_g", "sum_b", "sum_x", "sum_y")]
+                means_of[l] = ([oracle.colour_mean(int(sp[f][l]), n) for f in ("sum_r", "sum_g", "sum_b")]
+                               + [oracle.round_mean(int(sp[f][l]), n) for f in ("sum_x", "sum_y")])
             means[c] = means_of[l]
         d = [1, int(im[y, x, 0]), int(im[y, x, 1]), int(im[y, x, 2]), x, y]
         code, B, _ = oracle.block_move(win, means, d, [1, 1, 1, 1], p)

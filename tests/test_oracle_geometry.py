@@ -100,6 +100,25 @@ def test_round_mean_exhaustive():
         assert oracle.round_mean(S, n) == brute.round_half_up(Fraction(S * 256, n))
 
 
+# ---------------------------------------------------------------- O5 + A33 (colour means)
+def test_colour_mean_clamped_to_intensity_range():
+    # inside [0, 255 n] the colour mean is O5's rounding; a constant region of intensity v has
+    # mean v exactly (v * 2^8); outside the range (literal pyramid data only) the mean is the
+    # nearest intensity bound, 0 or 255 (DESIGN A33)
+    for n in range(1, 25):
+        for v in (0, 1, 128, 254, 255):
+            assert oracle.colour_mean(v * n, n) == v << 8
+        for S in range(-3 * n, 258 * n, max(1, n // 2)):
+            exact = brute.round_half_up(Fraction(S * 256, n))
+            want = 0 if S < 0 else (255 << 8 if S > 255 * n else exact)
+            assert oracle.colour_mean(S, n) == want, (S, n)
+            if 0 <= S <= 255 * n:
+                assert oracle.colour_mean(S, n) == oracle.round_mean(S, n)
+    assert oracle.colour_mean(-1, 10**6) == 0                 # rounds to 0 anyway
+    assert oracle.colour_mean(255 * 7 + 1, 7) == 255 << 8      # just above the range
+    assert oracle.colour_mean(-(2**40), 3) == 0
+
+
 # ---------------------------------------------------------------- A9 (E_topo)
 def test_topology_lut_exhaustive_vs_flood_fill():
     accepted = 0

@@ -415,6 +415,7 @@ StageDev stage_dev(rapid_ctx *c, int s, int32_t *labels_out) {
   d.uniform = 1;
   for (size_t i = 0; i < S.xs.size() && d.uniform; i++) d.uniform = S.xs[i] == (int32_t)(i * S.b);
   for (size_t j = 0; j < S.ys.size() && d.uniform; j++) d.uniform = S.ys[j] == (int32_t)(j * S.b);
+  d.bsum32 = (S.b == 2 && d.uniform) ? 1 : 0;  // 2x2 sums fit 10 bits per channel
   d.fd_tx = make_fastdiv((uint32_t)S.tiles_x);
   d.fd_ty = make_fastdiv((uint32_t)S.tiles_y);
   d.fd_nbx = make_fastdivu((uint32_t)S.nbx);

@@ -73,7 +73,8 @@ struct StageDev {
   const int32_t *xs, *ys;        // block boundaries (nbx+1, nby+1)
   const int32_t *px, *py;        // parent block index in stage s-1 (s > 0)
   const int32_t *cxs, *cys;      // first child index in stage s+1 (nbx+1, nby+1)
-  const uint64_t *bsum;          // packed colour sums r | g<<21 | b<<42 (b > 1), else null
+  const uint64_t *bsum;          // packed colour sums r | g<<21 | b<<42 (b > 1), else null;
+  int32_t bsum32;                // 1: uniform b = 2 stage, sums stored as u32 r | g<<10 | b<<20 (<= 1020 each)
   int32_t *map;                  // stage label map [B][nby][nbx], per-image local ids
 };
 
@@ -264,6 +265,17 @@ __device__ __forceinline__ void agg_add_i32(bool valid, int key, int v, int32_t 
   if (valid && run.end) atomicAdd(&arr[key], s);
 }
 
+// packed colour sums of block idx in the u64 layout r | g<<21 | b<<42 (from either storage)
+__device__ __forceinline__ uint64_t widen_bsum32(uint32_t v) {
+  return (uint64_t)(v & 0x3FFu) | ((uint64_t)((v >> 10) & 0x3FFu) << 21) | ((uint64_t)(v >> 20) << 42);
+}
+__device__ __forceinline__ uint64_t bsum_at(const StageDev &st, size_t idx) {
+  return st.bsum32 ? widen_bsum32(reinterpret_cast<const uint32_t *>(st.bsum)[idx]) : st.bsum[idx];
+}
+__device__ __forceinline__ uint32_t narrow_bsum32(uint64_t pk) {
+  return (uint32_t)(pk & 0x3FFull) | ((uint32_t)((pk >> 21) & 0x3FFull) << 10) | ((uint32_t)((pk >> 42) & 0x3FFull) << 20);
+}
+
 // Block data of a block at stage `st`: n, colour sums, position sums (x = column).
 // Positions are closed-form sums over the block rectangle at full resolution (Eq. 8 exact).
 __device__ __forceinline__ void block_data_blk(const StageDev &st, int img, int gx, int gy,
@@ -271,7 +283,7 @@ __device__ __forceinline__ void block_data_blk(const StageDev &st, int img, int 
   const long long x0 = st.xs[gx], x1 = st.xs[gx + 1];
   const long long y0 = st.ys[gy], y1 = st.ys[gy + 1];
   const long long w = x1 - x0, h = y1 - y0;
-  const uint64_t pk = st.bsum[((size_t)img * st.nby + gy) * st.nbx + gx];
+  const uint64_t pk = bsum_at(st, ((size_t)img * st.nby + gy) * st.nbx + gx);
   d[0] = w * h;
   d[1] = (long long)(pk & 0x1FFFFFull);
   d[2] = (long long)((pk >> 21) & 0x1FFFFFull);

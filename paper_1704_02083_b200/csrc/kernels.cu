@@ -72,8 +72,10 @@ __global__ void k_pyramid_leaf(const StageDev st, const uint8_t *__restrict__ im
         sb += row[3 * x + 2];
       }
     }
-    const uint64_t pk = (uint64_t)sr | ((uint64_t)sg << 21) | ((uint64_t)sb << 42);
-    bsum[t] = literal ? lit_round(pk, (uint64_t)(x1 - x0) * (uint64_t)(y1 - y0)) : pk;
+    uint64_t pk = (uint64_t)sr | ((uint64_t)sg << 21) | ((uint64_t)sb << 42);
+    if (literal) pk = lit_round(pk, (uint64_t)(x1 - x0) * (uint64_t)(y1 - y0));
+    if (st.bsum32) reinterpret_cast<uint32_t *>(bsum)[t] = narrow_bsum32(pk);
+    else bsum[t] = pk;
   }
 }
 
@@ -109,9 +111,9 @@ __global__ void k_pyramid_leaf2(const StageDev st, const uint8_t *__restrict__ i
       out[j] = (uint64_t)s[0] | ((uint64_t)s[1] << 21) | ((uint64_t)s[2] << 42);
       if (literal) out[j] = lit_round(out[j], 4);
     }
-    uint64_t *dst = bsum + row * st.nbx + gx;
-    reinterpret_cast<ulonglong2 *>(dst)[0] = make_ulonglong2(out[0], out[1]);
-    reinterpret_cast<ulonglong2 *>(dst)[1] = make_ulonglong2(out[2], out[3]);
+    // uniform b = 2: u32 storage (StageDev::bsum32)
+    *reinterpret_cast<uint4 *>(reinterpret_cast<uint32_t *>(bsum) + row * st.nbx + gx) =
+        make_uint4(narrow_bsum32(out[0]), narrow_bsum32(out[1]), narrow_bsum32(out[2]), narrow_bsum32(out[3]));
   }
 }
 
@@ -154,32 +156,13 @@ __global__ void k_pyramid_leaf24(const StageDev st, const StageDev up, const uin
         if (literal) o2[h][j] = lit_round(o2[h][j], 4);
       }
     }
-    // stores: every store instruction of the warp writes whole 32-B sectors (a half-sector
-    // write costs a DRAM read-modify-write).  When the warp's 32 threads are 32 consecutive
-    // groups of one block-row pair, its output rows are contiguous 1-KB runs: lane i stores the
-    // 16 B at offset 16 i, i.e. pair (i & 1) of lane 16 * half + i / 2.
-    const bool contiguous = base + 31 < n && (base / q) == ((base + 31) / q);
+    // b = 2 sums in u32 storage (StageDev::bsum32): a thread's four blocks are 16 contiguous
+    // bytes, so the lanes of a warp on one block row write whole 32-B sectors
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
-      if (contiguous) {
-        const size_t pr0 = base / q;
-        const int img0 = (int)(pr0 / npair), gy0 = 2 * (int)(pr0 - (size_t)img0 * npair);
-        uint64_t *row = bsum + ((size_t)img0 * st.nby + gy0 + h) * st.nbx + (size_t)(base - pr0 * q) * 4;
-#pragma unroll
-        for (int half = 0; half < 2; half++) {
-          const int src = 16 * half + (int)(lane >> 1);
-          const uint64_t a0 = __shfl_sync(0xffffffffu, o2[h][0], src), a1 = __shfl_sync(0xffffffffu, o2[h][1], src);
-          const uint64_t a2 = __shfl_sync(0xffffffffu, o2[h][2], src), a3 = __shfl_sync(0xffffffffu, o2[h][3], src);
-          const bool hi = lane & 1u;
-          *reinterpret_cast<ulonglong2 *>(row + 4 * (size_t)src + (hi ? 2 : 0)) =
-              hi ? make_ulonglong2(a2, a3) : make_ulonglong2(a0, a1);
-        }
-      } else if (valid) {
-        uint64_t *dst = bsum + ((size_t)img * st.nby + gy + h) * st.nbx + gx;
-        reinterpret_cast<ulonglong2 *>(dst)[0] = make_ulonglong2(o2[h][0], o2[h][1]);
-        reinterpret_cast<ulonglong2 *>(dst)[1] = make_ulonglong2(o2[h][2], o2[h][3]);
-      }
-    }
+    for (int h = 0; h < 2; h++)
+      if (valid)
+        *reinterpret_cast<uint4 *>(reinterpret_cast<uint32_t *>(bsum) + ((size_t)img * st.nby + gy + h) * st.nbx + gx) =
+            make_uint4(narrow_bsum32(o2[h][0]), narrow_bsum32(o2[h][1]), narrow_bsum32(o2[h][2]), narrow_bsum32(o2[h][3]));
     if (valid) {  // packed fields never carry: each stays < 2^21 up to b = 90
       uint64_t u0 = o2[0][0] + o2[0][1] + o2[1][0] + o2[1][1], u1 = o2[0][2] + o2[0][3] + o2[1][2] + o2[1][3];
       if (literal) {
@@ -204,7 +187,7 @@ __global__ void k_pyramid_up(const StageDev st, const StageDev ch, int B, uint64
     uint64_t acc = 0;
     for (int cy = st.cys[gy]; cy < st.cys[gy + 1]; cy++)
       for (int cx = st.cxs[gx]; cx < st.cxs[gx + 1]; cx++)
-        acc += ch.bsum[((size_t)img * ch.nby + cy) * ch.nbx + cx];
+        acc += bsum_at(ch, ((size_t)img * ch.nby + cy) * ch.nbx + cx);
     if (literal)
       acc = lit_round(acc, (uint64_t)(st.xs[gx + 1] - st.xs[gx]) * (uint64_t)(st.ys[gy + 1] - st.ys[gy]));
     bsum[t] = acc;

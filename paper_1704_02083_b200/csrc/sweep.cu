@@ -801,7 +801,9 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
           const uint8_t *p = a.image + (((size_t)img * a.H + gy) * a.W + gx) * 3;
           rgb = (uint32_t)__ldcs(p) | ((uint32_t)__ldcs(p + 1) << 8) | ((uint32_t)__ldcs(p + 2) << 16);
         } else {
-          pk = __ldcs(reinterpret_cast<const unsigned long long *>(st.bsum) + ((size_t)img * nby + gy) * nbx + gx);
+          const size_t bi = ((size_t)img * nby + gy) * nbx + gx;
+          pk = st.bsum32 ? widen_bsum32(__ldcs(reinterpret_cast<const unsigned *>(st.bsum) + bi))
+                         : __ldcs(reinterpret_cast<const unsigned long long *>(st.bsum) + bi);
           bx0 = st.xs[gx]; bx1 = st.xs[gx + 1];
           by0 = st.ys[gy]; by1 = st.ys[gy + 1];
         }

@@ -39,3 +39,27 @@ for name, fn, gb in (("h2d", h2d, n_in), ("d2h", d2h, n_out), ("both", lambda: (
     timed(fn)
     ms = min(timed(fn) for _ in range(3))
     print(f"{name}: {ms:.1f} ms, {gb / ms / 1e6:.1f} GB/s")
+
+# the same copies split over 2 / 4 streams (several copy engines at once?)
+for parts in (2, 4):
+    ss = [torch.cuda.Stream() for _ in range(parts)]
+
+    def d2h_split():
+        step = n_out // parts
+        for i, st in enumerate(ss):
+            with torch.cuda.stream(st):
+                ho[i * step:(i + 1) * step].copy_(do[i * step:(i + 1) * step], non_blocking=True)
+
+    def both_split():
+        with torch.cuda.stream(s1):
+            di.copy_(hi, non_blocking=True)
+        d2h_split()
+
+    for name, fn, gb in ((f"d2h x{parts}", d2h_split, n_out), (f"both (d2h x{parts})", both_split, n_in + n_out)):
+        def run(fn=fn):
+            fn()
+            for st in ss:
+                torch.cuda.current_stream().wait_stream(st)
+        timed(run)
+        ms = min(timed(run) for _ in range(3))
+        print(f"{name}: {ms:.1f} ms, {gb / ms / 1e6:.1f} GB/s")

@@ -163,6 +163,31 @@ __device__ __forceinline__ WarpRun warp_runs(bool valid, int key) {
   return r;
 }
 
+// Streaming (evict-first) loads that ask L2 for a 64-B fill: without the prefetch-size
+// qualifier an isolated load fetches 128 B from DRAM on this B200 (measured,
+// tools/micro/dram_granularity.cu: 128 B per scattered 4-B load by default, 64 B with
+// .L2::64B), which doubles the traffic of sparse 3x3 windows.
+__device__ __forceinline__ int ld_stream64(const int32_t *p) {
+  int v;
+  asm("ld.global.cs.L2::64B.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_stream64(const uint32_t *p) {
+  uint32_t v;
+  asm("ld.global.cs.L2::64B.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_stream64(const uint8_t *p) {
+  uint32_t v;
+  asm("ld.global.cs.L2::64B.u8 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_stream64(const unsigned long long *p) {
+  unsigned long long v;
+  asm("ld.global.cs.L2::64B.b64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
 // int64 atomic add that asks L2 to keep the line (evict_last): the per-superpixel sums are
 // the atomic targets of every phase and must not be displaced by the streaming label reads
 __device__ __forceinline__ void red_add_keep(unsigned long long *p, unsigned long long v) {

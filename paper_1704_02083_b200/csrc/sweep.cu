@@ -799,20 +799,20 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
         int bx0 = 0, bx1 = 1, by0 = 0, by1 = 1;
         if (PIXEL) {
           const uint8_t *p = a.image + (((size_t)img * a.H + gy) * a.W + gx) * 3;
-          rgb = (uint32_t)__ldcs(p) | ((uint32_t)__ldcs(p + 1) << 8) | ((uint32_t)__ldcs(p + 2) << 16);
+          rgb = ld_stream64(p) | (ld_stream64(p + 1) << 8) | (ld_stream64(p + 2) << 16);
         } else {
           const size_t bi = ((size_t)img * nby + gy) * nbx + gx;
-          pk = st.bsum32 ? widen_bsum32(__ldcs(reinterpret_cast<const unsigned *>(st.bsum) + bi))
-                         : __ldcs(reinterpret_cast<const unsigned long long *>(st.bsum) + bi);
+          pk = st.bsum32 ? widen_bsum32(ld_stream64(reinterpret_cast<const uint32_t *>(st.bsum) + bi))
+                         : ld_stream64(reinterpret_cast<const unsigned long long *>(st.bsum) + bi);
           bx0 = st.xs[gx]; bx1 = st.xs[gx + 1];
           by0 = st.ys[gy]; by1 = st.ys[gy + 1];
         }
         const int32_t *m = st.map + (size_t)img * nby * nbx;
         const size_t o = (size_t)gy * nbx + gx;
         const bool hN = gy > 0, hS = gy + 1 < nby, hW = gx > 0, hE = gx + 1 < nbx;
-        // streaming loads (evict-first): keep L2 for the per-superpixel tables
+        // streaming loads (evict-first, 64-B DRAM fill): keep L2 for the per-superpixel tables
 #ifndef RAPID_WLD
-#define RAPID_WLD __ldcs
+#define RAPID_WLD ld_stream64
 #endif
         A = RAPID_WLD(m + o);
         const int nq0 = hN ? RAPID_WLD(m + o - nbx) : -1, nq1 = hE ? RAPID_WLD(m + o + 1) : -1;

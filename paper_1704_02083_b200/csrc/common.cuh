@@ -188,6 +188,47 @@ __device__ __forceinline__ unsigned long long ld_stream64(const unsigned long lo
   return v;
 }
 
+// The same 64-B fill for gathers of the per-superpixel tables (records, sums, flags): coherent
+// loads (the table may have been written earlier in the same kernel), and non-coherent
+// read-only ones (.nc) where the kernel never writes it.
+__device__ __forceinline__ int4 ld64_v4(const void *p) {
+  int4 v;
+  asm("ld.global.L2::64B.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int4 ldnc64_v4(const void *p) {
+  int4 v;
+  asm("ld.global.nc.L2::64B.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ ulonglong2 ld64_v2u64(const void *p) {
+  ulonglong2 v;
+  asm("ld.global.L2::64B.v2.b64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld64_u32(const void *p) {
+  uint32_t v;
+  asm("ld.global.L2::64B.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld64_u8(const void *p) {
+  uint32_t v;
+  asm("ld.global.L2::64B.u8 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ldnc64_u32(const void *p) {
+  uint32_t v;
+  asm("ld.global.nc.L2::64B.b32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ Rec ldnc64_rec(const Rec *p) {
+  const int4 a = ldnc64_v4(p), b = ldnc64_v4(reinterpret_cast<const int4 *>(p) + 1);
+  Rec r;
+  r.mux = a.x; r.muy = a.y; r.cq01 = (uint32_t)a.z; r.cq2f = (uint32_t)a.w;
+  r.n = b.x; r.init = b.y; r.pad0 = b.z; r.pad1 = b.w;
+  return r;
+}
+
 // int64 atomic add that asks L2 to keep the line (evict_last): the per-superpixel sums are
 // the atomic targets of every phase and must not be displaced by the streaming label reads
 __device__ __forceinline__ void red_add_keep(unsigned long long *p, unsigned long long v) {

@@ -200,13 +200,17 @@ void launch_init_map0(const InitArgs &a, cudaStream_t s);
 void launch_stats0(const InitArgs &a, cudaStream_t s);
 // ------------------------------------------------------------------ K3: snapshot (device side)
 __device__ __forceinline__ void make_rec(const SpDev &sp, int k) {
-  const unsigned long long *s = sp.sums + (size_t)k * SUMW;
+  // gathers with a 64-B L2 fill (ld64_*, common.cuh); coherent: the fused commit + snapshot
+  // kernel reads sums its own atomics wrote
+  const ulonglong2 s01 = ld64_v2u64(sp.sums + (size_t)k * SUMW), s23 = ld64_v2u64(sp.sums + (size_t)k * SUMW + 2);
+  const ulonglong2 s45 = ld64_v2u64(sp.sums + (size_t)k * SUMW + 4);
+  const unsigned long long s[6] = {s01.x, s01.y, s23.x, s23.y, s45.x, s45.y};
   const unsigned long long n = s[0];
   Rec r;
   r.n = (int32_t)n;
-  r.init = sp.init[k];
-  const uint32_t flags = (uint32_t)sp.alive[k] | ((uint32_t)sp.active[k] << 1) |
-                         ((uint32_t)(sp.y[k] + 1) << 2);
+  r.init = (int32_t)ld64_u32(sp.init + k);
+  const uint32_t flags = ld64_u8(sp.alive + k) | (ld64_u8(sp.active + k) << 1) |
+                         ((uint32_t)((int)(int8_t)ld64_u8(sp.y + k) + 1) << 2);
   uint32_t c0 = 0, c1 = 0, c2 = 0;
   int32_t mx = 0, my = 0;
   if (n > 0) {

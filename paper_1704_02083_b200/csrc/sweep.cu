@@ -861,10 +861,10 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
         Rec recA;
         int4 rn[4];
         const bool need_rn = bnd && (topo_ok || a.gating == 2);
-        if (bnd) recA = a.sp.rec[kb + A];
+        if (bnd) recA = ldnc64_rec(&a.sp.rec[kb + A]);
 #pragma unroll
         for (int k2 = 0; k2 < 4; k2++)
-          rn[k2] = (need_rn && k2 < nb) ? __ldg(reinterpret_cast<const int4 *>(&a.sp.rec[kb + cb[k2]]))
+          rn[k2] = (need_rn && k2 < nb) ? ldnc64_v4(&a.sp.rec[kb + cb[k2]])
                                         : make_int4(0, 0, 0, 0);
         bool keep = bnd;
         if (bnd && a.gating == 1) keep = ((recA.cq2f >> 16) & F_ACTIVE) != 0u;
@@ -1020,9 +1020,10 @@ __global__ void __launch_bounds__(256) k_commit(const PhaseArgs a) {
       } else {
         block_data_blk(a.st, img, gx, gy, d);
       }
-      const Rec ra = a.sp.rec[kb + A];
+      const int4 rb = ldnc64_v4(reinterpret_cast<const int4 *>(&a.sp.rec[kb + A]) + 1);  // n, init
+      const int outA = (int)ldnc64_u32(&a.sp.out[kb + A]);
       // O6' all-or-nothing budget: the total proposed outflow must keep A >= l * InitSize (A19)
-      ok = !(((long long)ra.n - (long long)a.sp.out[kb + A]) * a.l_den < a.l_num * (long long)ra.init);
+      ok = !(((long long)rb.x - (long long)outA) * a.l_den < a.l_num * (long long)rb.y);
       if (ok) {
         a.st.map[idx] = B;
         if (a.bset) bset_insert(a.bset, a.st, img, gx, gy, pr.w >> 24);

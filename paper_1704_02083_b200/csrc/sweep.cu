@@ -759,7 +759,7 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
       const uint32_t rr = fdiv(t, st.fd_tx), img = fdiv(rr, st.fd_ty);
       const int gx0 = (int)(t - rr * (uint32_t)st.tiles_x) * TX, gy0 = (int)(rr - img * (uint32_t)st.tiles_y) * TY;
       widx = t * BSET_WORDS_PER_TILE + (uint32_t)(colour * (TY / 2) + (q & 7));
-      word = a.bset[widx];
+      word = ld64_u32(a.bset + widx);  // 64-B fill: the phase needs 32 B of the tile's 128
       wpos = (uint32_t)(gx0 + a.cx) | ((uint32_t)(gy0 + 2 * (q & 7) + a.cy) << 16);
       wimg = (int)img;
     }

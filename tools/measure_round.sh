@@ -31,9 +31,12 @@ json.dump({"kernel": "k_sweep<true,true,4> (K4), config 4 pixel stage, all %d la
            "dram_bytes_per_launch": (sum(rd) + sum(wr)) / n,
            "dram_bytes_per_launch_each": [a + b for a, b in zip(rd, wr)]},
           open("profiles/sweep_traffic.json", "w"), indent=1)
+# (profiles/ does not travel back from a gpurun box: the CSV under gpurun_out/ does, and
+#  re-running this block locally on it regenerates the same JSON)
 print("traffic per launch (mean of %d): %.0f B" % (n, (sum(rd) + sum(wr)) / n))
 PY
 cp $OUT/${TAG}_sweep_dram.csv profiles/${TAG}_sweep_dram.csv
+cp profiles/sweep_traffic.json $OUT/${TAG}_sweep_traffic.json
 # 2. bench
 python bench.py > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err || tail -5 $OUT/${TAG}_bench.err
 cp $OUT/${TAG}_bench.json profiles/${TAG}_bench_cfg4.json

@@ -858,14 +858,6 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   int rc = cuda_check(c, cudaSetDevice(device), "cudaSetDevice");
   if (rc) { delete c; return rc; }
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
-  if (const char *e = getenv("RAPID_L2_FETCH")) {  // A/B: cudaLimitMaxL2FetchGranularity (bytes)
-    size_t before = 0, after = 0;
-    cudaDeviceGetLimit(&before, cudaLimitMaxL2FetchGranularity);
-    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e));
-    cudaDeviceGetLimit(&after, cudaLimitMaxL2FetchGranularity);
-    if (getenv("RAPID_VERBOSE")) fprintf(stderr, "rapid: L2 fetch granularity %zu -> %zu\n", before, after);
-    cudaGetLastError();
-  }
   const size_t K = max_superpixels_total;
   size_t hc = 1024;
   while (hc < 12 * K + 1024) hc <<= 1;  // planar adjacency: <= 3K unordered pairs, 2 directions

@@ -994,7 +994,7 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
 // SNAP (cooperative launch, every CTA resident): after a grid barrier the same CTAs refresh the
 // records this commit stamped dirty (K3 of the next phase / of the stage end, without a launch)
 template <bool PIXEL, bool SNAP>
-__global__ void __launch_bounds__(256) k_commit(const PhaseArgs a) {
+__global__ void __launch_bounds__(256, 8) k_commit(const PhaseArgs a) {  // 8 CTAs/SM: the grid is one wave
   const unsigned long long n = cta_count(a.prev, a.prop_count, !SNAP);
   if (n == 0) return;  // SNAP: grid-uniform (an empty list stamps nothing to refresh)
   unsigned c_commit = 0, c_rej = 0;

@@ -1205,9 +1205,40 @@ void launch_pyramid_leaf(const StageDev &st, const uint8_t *image, int H, int W,
     k_pyramid_leaf<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(st, image, H, W, B, bsum, literal);
 }
 
+// Dyadic parent level (both uniform, b_parent = 2 b_child, child sums in u64 storage): a thread
+// forms two adjacent parents of one row from two 32-B child runs (two child rows x four
+// children), with 16-B loads and one 16-B store.
+template <bool literal>
+__global__ void k_pyramid_up2(const StageDev st, const StageDev ch, int B, uint64_t *__restrict__ bsum) {
+  const int q = st.nbx / 2;  // parent pairs per row
+  const size_t n = (size_t)q * st.nby * B;
+  const uint64_t area = (uint64_t)st.b * (uint64_t)st.b;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = t / q;  // img * nby + gy
+    const int gx = 2 * (int)(t - row * q);
+    const int img = (int)(row / st.nby), gy = (int)(row - (size_t)img * st.nby);
+    const uint64_t *c0 = ch.bsum + ((size_t)img * ch.nby + 2 * gy) * ch.nbx + 2 * gx;
+    const uint64_t *c1 = c0 + ch.nbx;
+    const ulonglong2 a0 = __ldcs(reinterpret_cast<const ulonglong2 *>(c0)), a1 = __ldcs(reinterpret_cast<const ulonglong2 *>(c0) + 1);
+    const ulonglong2 b0 = __ldcs(reinterpret_cast<const ulonglong2 *>(c1)), b1 = __ldcs(reinterpret_cast<const ulonglong2 *>(c1) + 1);
+    uint64_t u0 = a0.x + a0.y + b0.x + b0.y, u1 = a1.x + a1.y + b1.x + b1.y;  // fields never carry
+    if (literal) {
+      u0 = lit_round(u0, area);
+      u1 = lit_round(u1, area);
+    }
+    *reinterpret_cast<ulonglong2 *>(bsum + row * st.nbx + gx) = make_ulonglong2(u0, u1);
+  }
+}
+
 void launch_pyramid_up(const StageDev &parent, const StageDev &child, int B, uint64_t *bsum, bool literal,
                        cudaStream_t s) {
   const size_t n = (size_t)parent.nbx * parent.nby * B;
+  if (parent.uniform && child.uniform && parent.b == 2 * child.b && !child.bsum32 && parent.nbx % 2 == 0 &&
+      child.nbx == 2 * parent.nbx && child.nby == 2 * parent.nby) {
+    if (literal) k_pyramid_up2<true><<<grid_for(n / 2, 256, 148 * 16), 256, 0, s>>>(parent, child, B, bsum);
+    else k_pyramid_up2<false><<<grid_for(n / 2, 256, 148 * 16), 256, 0, s>>>(parent, child, B, bsum);
+    return;
+  }
   k_pyramid_up<<<grid_for(n, 256, 148 * 32), 256, 0, s>>>(parent, child, B, bsum, literal);
 }
 

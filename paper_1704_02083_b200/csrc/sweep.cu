@@ -621,21 +621,36 @@ __global__ void __launch_bounds__(K4A_THREADS) k_tiles(const PhaseArgs a, const 
       const int Wn = mid[2 * lane - 1], En = mid[2 * lane + 2];
       const int L[2] = {Mv.x, Mv.y}, N[2] = {U.x, U.y}, S[2] = {D.x, D.y}, Wv[2] = {Wn, Mv.x}, Ev[2] = {Mv.y, En};
       bool bnd[2];
+      if (!inf.w) {  // interior tile (warp-uniform): no "no block" marks in the box
 #pragma unroll
-      for (int c = 0; c < 2; c++)
-        bnd[c] = L[c] >= 0 && ((N[c] >= 0 && N[c] != L[c]) | (S[c] >= 0 && S[c] != L[c]) |
-                               (Wv[c] >= 0 && Wv[c] != L[c]) | (Ev[c] >= 0 && Ev[c] != L[c]));
+        for (int c = 0; c < 2; c++)
+          bnd[c] = (N[c] != L[c]) | (S[c] != L[c]) | (Wv[c] != L[c]) | (Ev[c] != L[c]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 2; c++)
+          bnd[c] = L[c] >= 0 && ((N[c] >= 0 && N[c] != L[c]) | (S[c] >= 0 && S[c] != L[c]) |
+                                 (Wv[c] >= 0 && Wv[c] != L[c]) | (Ev[c] >= 0 && Ev[c] != L[c]));
+      }
       if (OP == TILE_BSET) {
-        bool bit[2];
-#pragma unroll
-        for (int c = 0; c < 2; c++) {
-          bit[c] = bnd[c];
-          if (bnd[c] && a.gating == 1) {
-            if (kb + L[c] != last) {  // cache keyed by the global id (images share local ids)
-              last = kb + L[c];
-              last_flag = a.sp.active[kb + L[c]] != 0;
-            }
-            bit[c] = last_flag;
+        bool bit[2] = {bnd[0], bnd[1]};
+        if (a.gating == 1) {
+          // static gate: the active flags of both columns' labels, looked up together (at most
+          // two independent loads) unless the lane's cached label (keyed by the global id:
+          // images share local ids) or the other column already has it
+          const int g0 = kb + L[0], g1 = kb + L[1];
+          const bool m0 = bnd[0] && g0 != last;
+          const bool m1 = bnd[1] && g1 != last && !(m0 && g1 == g0);
+          const bool f0 = m0 && a.sp.active[g0] != 0, f1 = m1 && a.sp.active[g1] != 0;
+          const bool a0 = m0 ? f0 : last_flag;
+          const bool a1 = m1 ? f1 : ((m0 && g1 == g0) ? a0 : last_flag);
+          bit[0] = bnd[0] && a0;
+          bit[1] = bnd[1] && a1;
+          if (bnd[1]) {
+            last = g1;
+            last_flag = a1;
+          } else if (bnd[0]) {
+            last = g0;
+            last_flag = a0;
           }
         }
         const unsigned w0 = __ballot_sync(FULL, bit[0]), w1 = __ballot_sync(FULL, bit[1]);

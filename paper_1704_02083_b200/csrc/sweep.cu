@@ -539,6 +539,25 @@ __global__ void __launch_bounds__(256) k_bset_build(const PhaseArgs a) {
 //              lengths to the (victim, neighbour) hash.
 constexpr int TILE_BSET = 0, TILE_ADJ = 1;
 
+// The u8 flags of the labels of a lane's two columns (b0/b1: whether each is needed), looked up
+// together — at most two independent loads — unless the lane's cached label (keyed by the global
+// id: images share local ids) or the other column already has it; the cache keeps the last one.
+__device__ __forceinline__ void flag_pair(const uint8_t *flags, bool b0, bool b1, int g0, int g1, int &last,
+                                          bool &last_flag, bool &a0, bool &a1) {
+  const bool m0 = b0 && g0 != last;
+  const bool m1 = b1 && g1 != last && !(m0 && g1 == g0);
+  const bool f0 = m0 && flags[g0] != 0, f1 = m1 && flags[g1] != 0;
+  a0 = m0 ? f0 : last_flag;
+  a1 = m1 ? f1 : ((m0 && g1 == g0) ? a0 : last_flag);
+  if (b1) {
+    last = g1;
+    last_flag = a1;
+  } else if (b0) {
+    last = g0;
+    last_flag = a0;
+  }
+}
+
 template <int OP>
 __global__ void __launch_bounds__(K4A_THREADS) k_tiles(const PhaseArgs a, const MergeArgs ma,
                                                        const __grid_constant__ CUtensorMap tmap) {
@@ -633,25 +652,11 @@ __global__ void __launch_bounds__(K4A_THREADS) k_tiles(const PhaseArgs a, const 
       }
       if (OP == TILE_BSET) {
         bool bit[2] = {bnd[0], bnd[1]};
-        if (a.gating == 1) {
-          // static gate: the active flags of both columns' labels, looked up together (at most
-          // two independent loads) unless the lane's cached label (keyed by the global id:
-          // images share local ids) or the other column already has it
-          const int g0 = kb + L[0], g1 = kb + L[1];
-          const bool m0 = bnd[0] && g0 != last;
-          const bool m1 = bnd[1] && g1 != last && !(m0 && g1 == g0);
-          const bool f0 = m0 && a.sp.active[g0] != 0, f1 = m1 && a.sp.active[g1] != 0;
-          const bool a0 = m0 ? f0 : last_flag;
-          const bool a1 = m1 ? f1 : ((m0 && g1 == g0) ? a0 : last_flag);
+        if (a.gating == 1) {  // static gate: the labels' active flags
+          bool a0, a1;
+          flag_pair(a.sp.active, bnd[0], bnd[1], kb + L[0], kb + L[1], last, last_flag, a0, a1);
           bit[0] = bnd[0] && a0;
           bit[1] = bnd[1] && a1;
-          if (bnd[1]) {
-            last = g1;
-            last_flag = a1;
-          } else if (bnd[0]) {
-            last = g0;
-            last_flag = a0;
-          }
         }
         const unsigned w0 = __ballot_sync(FULL, bit[0]), w1 = __ballot_sync(FULL, bit[1]);
         if (lane == 0) {
@@ -663,14 +668,11 @@ __global__ void __launch_bounds__(K4A_THREADS) k_tiles(const PhaseArgs a, const 
         }
       } else {  // TILE_ADJ
         const int gy = gy0 + rr;
+        bool vic[2];  // the labels' victim flags
+        flag_pair(ma.sp.victim, bnd[0], bnd[1], kb + L[0], kb + L[1], last, last_flag, vic[0], vic[1]);
 #pragma unroll
         for (int c = 0; c < 2; c++) {
-          if (!bnd[c]) continue;
-          if (kb + L[c] != last) {
-            last = kb + L[c];
-            last_flag = ma.sp.victim[kb + L[c]] != 0;
-          }
-          if (!last_flag) continue;
+          if (!bnd[c] || !vic[c]) continue;
           const int gx = gx0 + 2 * lane + c;
           const unsigned ew = (unsigned)(st.xs[gx + 1] - st.xs[gx]), eh = (unsigned)(st.ys[gy + 1] - st.ys[gy]);
           const int nq[4] = {N[c], Ev[c], S[c], Wv[c]};

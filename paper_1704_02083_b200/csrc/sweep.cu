@@ -1135,7 +1135,7 @@ void launch_eval(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
 // registers), the block stages at 3 (80; their 64-bit position sums spill at 64).
 // RAPID_SWEEP_MINB=2..4 forces one budget for every stage (A/B testing).
 static int g_sweep_minb = 0;
-static int g_sweep_minb_small = 3;  // RAPID_SWEEP_MINB_SMALL: CTAs/SM of the small-block variant
+static int g_sweep_minb_small = 4;  // RAPID_SWEEP_MINB_SMALL: CTAs/SM of the small-block variant (4: 64 registers, a few bytes of spill, -0.1 ms)
 
 template <int MB>
 static int sweep_occ() {

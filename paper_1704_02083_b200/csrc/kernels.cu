@@ -962,12 +962,15 @@ __global__ void __launch_bounds__(128) k_transition_dyadic(const TransArgs a) {
     const uint32_t rr = fdiv(t, nx.fd_tx), img = fdiv(rr, nx.fd_ty);
     const int tpx = (int)(t - rr * (uint32_t)nx.tiles_x) * (TX / 2), tpy = (int)(rr - img * (uint32_t)nx.tiles_y) * (TY / 2);
     const int kb = (int)img * a.M;
-    auto res = [&](int p) { return (p >= 0 && rm && !a.sp.alive[kb + p]) ? a.sp.remap[kb + p] : p; };
+    // flag / remap gathers with a 64-B L2 fill (scattered: a plain load fills 128 B)
+    auto res = [&](int p) {
+      return (p >= 0 && rm && !ld64_u8(a.sp.alive + kb + p)) ? (int)ld64_u32(a.sp.remap + kb + p) : p;
+    };
     p0 = res(p0);
     p1 = res(p1);
     const bool need_act = a.gate || (BSET && a.gating == 1);
-    const int a0 = (p0 >= 0 && need_act) ? a.sp.active[kb + p0] : 0;
-    const int a1 = (p1 >= 0 && need_act) ? a.sp.active[kb + p1] : 0;
+    const int a0 = (p0 >= 0 && need_act) ? (int)ld64_u8(a.sp.active + kb + p0) : 0;
+    const int a1 = (p1 >= 0 && need_act) ? (int)ld64_u8(a.sp.active + kb + p1) : 0;
     if (BSET) {  // remapped parents and halo into shared memory
       s_lab[r + 1][1 + 2 * q] = p0;
       s_lab[r + 1][2 + 2 * q] = p1;
@@ -979,7 +982,8 @@ __global__ void __launch_bounds__(128) k_transition_dyadic(const TransArgs a) {
         else { hy = u - 72; hx = 32; }
         const int y = tpy + hy, x = tpx + hx;
         int v = -1;
-        if (y >= 0 && y < pv.nby && x >= 0 && x < pv.nbx) v = res(pv.map[((size_t)img * pv.nby + y) * pv.nbx + x]);
+        if (y >= 0 && y < pv.nby && x >= 0 && x < pv.nbx)
+          v = res((int)ld64_u32(pv.map + ((size_t)img * pv.nby + y) * pv.nbx + x));
         s_lab[hy + 1][hx + 1] = v;
       }
     }

@@ -664,7 +664,6 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           pa.cnt = &ctl->cnt[st][t][ph][0];
           pa.prev = t > 0 ? &ctl->cnt[st][t - 1][0][0] : nullptr;
           pa.victim_any = &ctl->victim_any[st];
-          if (gated_sz) cudaMemsetAsync(c->out, 0, sizeof(int32_t) * K, s);
           if (c->use_bset) {
             Timer t2(c, s, RAPID_K_PROPOSE, st);
             launch_sweep(pa, pixel, P.st[st].smallb, c->sm_count, s);

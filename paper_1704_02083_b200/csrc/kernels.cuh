@@ -290,7 +290,11 @@ __device__ __forceinline__ void snapshot_warps(const SnapArgs &a, int wid, int n
           r--;
         }
         bit = __ffs(mm) - 1;
-        make_rec(a.sp, 4 * (ch * 32 + j) + bit);
+        const int k = 4 * (ch * 32 + j) + bit;
+        make_rec(a.sp, k);
+        // the proposed outflow of the next phase starts at zero: every superpixel whose
+        // out[] the last phase raised (every proposal's source) was stamped dirty by K5
+        a.sp.out[k] = 0;
       }
     }
   }

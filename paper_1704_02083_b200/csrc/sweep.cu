@@ -1047,6 +1047,7 @@ __global__ void __launch_bounds__(256, 8) k_commit(const PhaseArgs a) {  // 8 CT
       } else {
         rej = true;
         for (int f = 0; f < 6; f++) d[f] = 0;
+        a.sp.dirty[kb + A] = a.stamp;  // so that the next K3 resets out[A] (and re-derives A's record)
         if (a.size_mode == 2) {
           a.sp.victim[kb + A] = 1;
           *a.victim_any = 1u;

@@ -99,6 +99,7 @@ struct rapid_ctx {
   DevBuf himg, hlab;
   // occupancy
   int scan_grid = 0, eval_grid = 0, sweep_grid = 0, tiles_grid = 0;  // persistent grid sizes (CTAs)
+  int sweep_tail = 25;  // RAPID_SWEEP_TAIL: % of K4's words dealt in quarter-size groups at the end (block stages)
   int sweep_gpw = 2;  // K4 word groups per warp (RAPID_SWEEP_GPW overrides, A/B testing)
   bool fuse_snap = false;  // RAPID_FUSE_SNAP=1: K3 of the next phase runs at the end of a cooperative K5 (measured: same step time)
   bool fuse_bset = false;  // RAPID_FUSE_BSET=1: dyadic transitions also write the next stage's boundary sets (measured: no faster than the separate pass)
@@ -650,6 +651,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           pa.bset = c->use_bset ? (uint32_t *)c->bset.p : nullptr;
           pa.wq = &ctl->wq[g];
           pa.gpw = c->sweep_gpw;
+          pa.tail_pct = pixel ? 0 : c->sweep_tail;  // measured: helps the latency-bound block stages only
           pa.size_mode = (int)p->size_mode;
           pa.l_num = p->l_num; pa.l_den = p->l_den;
           pa.lam_pos = p->lambda_pos_q16;
@@ -886,6 +888,7 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   c->eval_grid = c->sm_count * eval_occupancy();
   c->sweep_grid = c->sm_count * sweep_occupancy();
   if (const char *e = getenv("RAPID_SWEEP_GPW")) c->sweep_gpw = std::max(1, atoi(e));
+  if (const char *e = getenv("RAPID_SWEEP_TAIL")) c->sweep_tail = std::min(100, std::max(0, atoi(e)));
   if (const char *e = getenv("RAPID_FUSE_BSET")) c->fuse_bset = e[0] == '1';
   if (const char *e = getenv("RAPID_FUSE_SNAP")) c->fuse_snap = e[0] == '1';
   c->tiles_grid = c->sm_count * tiles_occupancy();

@@ -27,6 +27,7 @@ struct PhaseArgs {
   uint32_t *victim_any;
   uint32_t *bset;            // boundary sets of the stage (null: full-scan path K4a/K4b)
   int32_t gpw;               // k_sweep: word groups per warp to aim for (sizes the groups)
+  int32_t tail_pct;          // k_sweep: % of the words dealt in quarter-size groups at the end
   unsigned int *wq;          // k_sweep: work-queue counter of this phase (zeroed per call)
 };
 

@@ -748,7 +748,13 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
   // queue's same-address atomics (measured: gpw 2 best at config 4)
   unsigned G = 32;
   while (G > 4 && ntiles * (TY / 2) / G < (unsigned)a.gpw * nw) G >>= 1;
-  const unsigned ngroups = (ntiles * (TY / 2) + G - 1) / G;
+  // the last tail_pct % of the words go out in groups of G/4 (>= 4): a shorter tail when the
+  // queue runs dry (the kernel ends with its slowest warp)
+  const unsigned nwords = ntiles * (TY / 2);
+  const unsigned Gt = G >= 16 ? G / 4 : 4;
+  const unsigned nhead = (unsigned)(((unsigned long long)nwords * (100u - (unsigned)a.tail_pct) / 100u) / G);
+  const unsigned head_words = nhead * G;
+  const unsigned ngroups = nhead + (nwords - head_words + Gt - 1) / Gt;
   const int colour = a.cx | (a.cy << 1);
   __shared__ unsigned s_cnt[5];  // cand, topo, prop, srej, commit (per CTA; flushed at the end)
   __shared__ uint32_t s_simple[8];  // 256-bit truth table of simple_point (E_topo) by ring mask
@@ -768,10 +774,11 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
     g = __shfl_sync(FULL, g, 0);
     if (g >= ngroups) break;
     // ---- this lane's word
-    const unsigned q = g * G + (unsigned)lane, w = q >> 3;  // (tile slot, plane row q % 8)
+    const unsigned gsz = g < nhead ? G : Gt;
+    const unsigned q = (g < nhead ? g * G : head_words + (g - nhead) * Gt) + (unsigned)lane, w = q >> 3;  // (tile slot, plane row q % 8)
     uint32_t word = 0, wpos = 0, widx = 0;
     int wimg = 0;
-    if ((unsigned)lane < G && w < ntiles) {
+    if ((unsigned)lane < gsz && w < ntiles) {
       const uint32_t t = a.worklist ? (uint32_t)a.worklist[w] : w;
       const uint32_t rr = fdiv(t, st.fd_tx), img = fdiv(rr, st.fd_ty);
       const int gx0 = (int)(t - rr * (uint32_t)st.tiles_x) * TX, gy0 = (int)(rr - img * (uint32_t)st.tiles_y) * TY;

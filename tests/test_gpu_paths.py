@@ -30,7 +30,8 @@ def make_ctx(env, pixels, sps):
                 os.environ[k] = v
 
 
-VARIANTS = [{}, {"RAPID_NO_GRAPH": "1"}, {"RAPID_SWEEP": "scan"}, {"RAPID_FUSE_BSET": "1"}, {"RAPID_FUSE_SNAP": "1"}]
+VARIANTS = [{}, {"RAPID_NO_GRAPH": "1"}, {"RAPID_SWEEP": "scan"}, {"RAPID_FUSE_BSET": "1"}, {"RAPID_FUSE_SNAP": "1"},
+            {"RAPID_NO_TMA": "1"}]
 
 
 @pytest.mark.parametrize("cfg,side", [(2, 1024), (4, 1024), (5, 0)])

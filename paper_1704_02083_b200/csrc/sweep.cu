@@ -948,13 +948,17 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
               } else {
                 prop = true;
                 Bm = bestB;
-                // neighbours that become boundary blocks if the move commits: label != B and
-                // passing the static gate (A passed it; others from their record flags)
-                ins = maskA;
-#pragma unroll
-                for (int k2 = 0; k2 < 4; k2++)
-                  if (k2 < nb && cb[k2] != Bm && (a.gating != 1 || (((unsigned)rn[k2].w >> 16) & F_ACTIVE)))
-                    ins |= cm[k2];
+                // neighbours whose boundary-set bit the move may have to set: only those labelled
+                // A (they now touch B); a neighbour of another label C != B already touched p's
+                // A, so it was a boundary block and its bit is set (invariant; A passed the gate
+                // and C's bit is needed only if C does).  An A-neighbour q is skipped too when a
+                // diagonal of p — q's other 4-neighbour across the row or column, a colour that
+                // does not move in this phase — holds another label: q was already a boundary block.
+                const bool oNE = dNE >= 0 && dNE != A, oSE = dSE >= 0 && dSE != A;
+                const bool oSW = dSW >= 0 && dSW != A, oNW = dNW >= 0 && dNW != A;
+                const unsigned known = ((unsigned)(oNW | oNE)) | ((unsigned)(oNE | oSE) << 1) |
+                                       ((unsigned)(oSW | oSE) << 2) | ((unsigned)(oNW | oSW) << 3);
+                ins = maskA & ~known;
               }
             }
           }

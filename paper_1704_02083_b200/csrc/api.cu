@@ -102,6 +102,7 @@ struct rapid_ctx {
   int sweep_tail = 25;  // RAPID_SWEEP_TAIL: % of K4's words dealt in quarter-size groups at the end (block stages)
   int sweep_gpw = 2;  // K4 word groups per warp (RAPID_SWEEP_GPW overrides, A/B testing)
   bool fuse_snap = false;  // RAPID_FUSE_SNAP=1: K3 of the next phase runs at the end of a cooperative K5 (measured: same step time)
+  bool bset_parent = true;  // dyadic stages: boundary sets from the parent map (RAPID_BSET_PARENT=0: child-map tile pass)
   bool fuse_bset = false;  // RAPID_FUSE_BSET=1: dyadic transitions also write the next stage's boundary sets (measured: no faster than the separate pass)
   bool use_bset = true;  // RAPID_SWEEP=scan selects the full-scan path K4a + K4b (A/B testing)
   // CUDA graph of the whole segmentation (one launch per call): captured on a private stream,
@@ -594,6 +595,11 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       ta.bset = (c->use_bset && c->fuse_bset) ? (uint32_t *)c->bset.p : nullptr;
       ta.gating = gating;
       bset_done = launch_transition(ta, s);
+      if (!bset_done && c->use_bset && c->bset_parent) {  // boundary sets from the parent map
+        ta.bset = (uint32_t *)c->bset.p;
+        bset_done = launch_bset_dyadic(ta, c->sm_count, s);
+        if (bset_done) c->launches++;
+      }
       c->launches++;
       if (p->stats_mode == RAPID_STATS_RECOUNT) {
         RecountArgs ra;
@@ -890,6 +896,7 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   if (const char *e = getenv("RAPID_SWEEP_GPW")) c->sweep_gpw = std::max(1, atoi(e));
   if (const char *e = getenv("RAPID_SWEEP_TAIL")) c->sweep_tail = std::min(100, std::max(0, atoi(e)));
   if (const char *e = getenv("RAPID_FUSE_BSET")) c->fuse_bset = e[0] == '1';
+  if (const char *e = getenv("RAPID_BSET_PARENT")) c->bset_parent = e[0] != '0';
   if (const char *e = getenv("RAPID_FUSE_SNAP")) c->fuse_snap = e[0] == '1';
   c->tiles_grid = c->sm_count * tiles_occupancy();
   {

@@ -1043,6 +1043,69 @@ __global__ void __launch_bounds__(128) k_transition_dyadic(const TransArgs a) {
   }
 }
 
+// Boundary sets of a dyadic stage from its parents (both stages uniform, b_prev = 2 b_next):
+// a child's 4-neighbours are its sibling pair (same parent, same label) and the children of
+// its parent's W/E and N/S neighbours on its side, so child (2px + cx, 2py + cy) is a boundary
+// block iff its parent's label differs from the parent neighbour on side cx horizontally or
+// cy vertically (labels after the pending remap, exactly the child map's values).  One CTA per
+// worklist tile of the child stage, warp w = plane row w, lane i = parent column tx*32 + i:
+// the four colour words of the row are four ballots.  Reads a quarter of the bytes of the
+// child-map tile pass (k_tiles<BSET>) with a fraction of its instructions.
+__global__ void __launch_bounds__(256) k_bset_dyadic(const TransArgs a) {
+  const StageDev &pv = a.prev, &nx = a.next;
+  const unsigned ntiles = a.gate ? *a.nwork : (unsigned)(nx.tiles_x * nx.tiles_y) * (unsigned)a.B;
+  const bool rm = *a.remap_pending != 0u;
+  const int lane = lane_id(), pr = threadIdx.x >> 5;
+  for (unsigned w = blockIdx.x; w < ntiles; w += gridDim.x) {
+    const uint32_t t = a.gate ? (uint32_t)a.worklist[w] : w;
+    const uint32_t rr = fdiv(t, nx.fd_tx), img = fdiv(rr, nx.fd_ty);
+    const int px = (int)(t - rr * (uint32_t)nx.tiles_x) * (TX / 2) + lane;
+    const int py = (int)(rr - img * (uint32_t)nx.tiles_y) * (TY / 2) + pr;
+    const int kb = (int)img * a.M;
+    const int32_t *pm = pv.map + (size_t)img * pv.nby * pv.nbx;
+    const bool in = px < pv.nbx && py < pv.nby;
+    auto res = [&](int p) {
+      return (p >= 0 && rm && !ld64_u8(a.sp.alive + kb + p)) ? (int)ld64_u32(a.sp.remap + kb + p) : p;
+    };
+    const size_t o = (size_t)py * pv.nbx + px;
+    int L = in ? pm[o] : -1;
+    int Nl = in && py > 0 ? pm[o - pv.nbx] : -1;
+    int Sl = in && py + 1 < pv.nby ? pm[o + pv.nbx] : -1;
+    int Wh = (lane == 0 && in && px > 0) ? pm[o - 1] : -1;          // halo (lane 0)
+    int Eh = (lane == 31 && in && px + 1 < pv.nbx) ? pm[o + 1] : -1;  // halo (lane 31)
+    L = res(L);
+    Nl = res(Nl);
+    Sl = res(Sl);
+    Wh = res(Wh);
+    Eh = res(Eh);
+    int Wl = __shfl_up_sync(FULL, L, 1), El = __shfl_down_sync(FULL, L, 1);
+    if (lane == 0) Wl = Wh;
+    if (lane == 31) El = Eh;
+    bool gate = L >= 0;
+    if (gate && a.gating == 1) gate = ld64_u8(a.sp.active + kb + L) != 0;
+    const bool dW = Wl >= 0 && Wl != L, dE = El >= 0 && El != L;
+    const bool dN = Nl >= 0 && Nl != L, dS = Sl >= 0 && Sl != L;
+    const unsigned w0 = __ballot_sync(FULL, gate && (dW || dN));  // (cx, cy) = (0, 0)
+    const unsigned w1 = __ballot_sync(FULL, gate && (dE || dN));  // (1, 0)
+    const unsigned w2 = __ballot_sync(FULL, gate && (dW || dS));  // (0, 1)
+    const unsigned w3 = __ballot_sync(FULL, gate && (dE || dS));  // (1, 1)
+    if (lane == 0) {
+      uint32_t *tw = a.bset + (size_t)t * 32 + pr;
+      tw[0 * (TY / 2)] = w0;
+      tw[1 * (TY / 2)] = w1;
+      tw[2 * (TY / 2)] = w2;
+      tw[3 * (TY / 2)] = w3;
+    }
+  }
+}
+
+bool launch_bset_dyadic(const TransArgs &a, int sms, cudaStream_t s) {
+  if (!(a.prev.uniform && a.next.uniform && a.prev.b == 2 * a.next.b && a.bset)) return false;
+  const unsigned ntiles = (unsigned)(a.next.tiles_x * a.next.tiles_y) * (unsigned)a.B;
+  k_bset_dyadic<<<std::min<unsigned>(ntiles, (unsigned)sms * 8), 256, 0, s>>>(a);
+  return true;
+}
+
 // ------------------------------------------------------------------ RECOUNT
 template <bool PIXEL>
 __global__ void k_recount(const RecountArgs a) {

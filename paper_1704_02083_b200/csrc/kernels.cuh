@@ -325,6 +325,9 @@ void launch_quality(const QualityArgs &a, int sms, cudaStream_t s);
 void launch_predict(const PredictArgs &a, int grid, cudaStream_t s, int *nlaunch);
 // returns true when it also wrote the boundary sets of `next` (dyadic path with a.bset)
 bool launch_transition(const TransArgs &a, cudaStream_t s);
+// boundary sets of a dyadic uniform stage from its parents' map (after the transition wrote the
+// child worklist); false when the stages are not dyadic uniform
+bool launch_bset_dyadic(const TransArgs &a, int sms, cudaStream_t s);
 void launch_recount(const RecountArgs &a, bool pixel, int grid, cudaStream_t s, int *nlaunch);
 void launch_final(const FinalArgs &a, bool upsample, cudaStream_t s);
 void launch_count_window(const StageDev &st, const SpDev &sp, int B, int M, unsigned long long *out,

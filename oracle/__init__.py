@@ -103,6 +103,7 @@ class OrcDebug(ctypes.Structure):
         ("phase_counters", ctypes.c_void_p),
         ("stage_victims", ctypes.c_int64 * MAX_STAGES),
         ("stage_merges", ctypes.c_int64 * MAX_STAGES),
+        ("victim_out", ctypes.c_void_p),
     ]
 
 
@@ -112,7 +113,8 @@ _LIB = None
 def lib():
     global _LIB
     if _LIB is None:
-        path = os.path.join(_HERE, "liboracle.so")
+        # RAPID_ORACLE_LIB: a mutated build for the mutation check (tools/mutation_check.sh)
+        path = os.environ.get("RAPID_ORACLE_LIB") or os.path.join(_HERE, "liboracle.so")
         if not os.path.exists(path):
             raise RuntimeError(f"{path} missing: run `make oracle`")
         L = ctypes.CDLL(path)
@@ -214,7 +216,9 @@ def segment(image, params, stop=None, log_moves=0, log_merges=0, map_cap=0):
         dbg.merges = merges.ctypes.data
         dbg.merges_cap = log_merges
     map_out = None
+    victims = np.zeros(B * M, dtype=np.uint8)
     if stop is not None:
+        dbg.victim_out = victims.ctypes.data
         dbg.stop_kind, dbg.stop_stage, dbg.stop_sweep, dbg.stop_phase = stop
         cap = map_cap or B * (H + 2) * (W + 2) * 2
         map_out = np.full(cap, -7, dtype=np.int32)
@@ -226,7 +230,9 @@ def segment(image, params, stop=None, log_moves=0, log_merges=0, map_cap=0):
         raise OracleError(rc)
     if map_out is not None and dbg.stopped:
         map_out = map_out[: B * dbg.map_nby * dbg.map_nbx].reshape(B, dbg.map_nby, dbg.map_nbx)
-    return Result(labels, sp, dbg, moves[: dbg.n_moves], merges[: dbg.n_merges], counters, map_out)
+    res = Result(labels, sp, dbg, moves[: dbg.n_moves], merges[: dbg.n_merges], counters, map_out)
+    res.victims = victims if (stop is not None and dbg.stopped) else None
+    return res
 
 
 class OracleError(RuntimeError):

@@ -303,6 +303,7 @@ static void dump_state(seg_t *g) {
   dbg->map_nby = st->nby;
   if (dbg->map_out && (int64_t)((g->img + 1) * per) <= dbg->map_cap)
     memcpy(dbg->map_out + (size_t)g->img * per, g->L, per * sizeof(int32_t));
+  if (dbg->victim_out) memcpy(dbg->victim_out + (size_t)g->img * g->M, g->victim, (size_t)g->M);
   dbg->stopped = 1;
 }
 

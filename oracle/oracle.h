@@ -91,6 +91,7 @@ typedef struct {
   int64_t *phase_counters;  /* [ORC_MAX_STAGES][ORC_MAX_SWEEPS][4][ORC_NCNT], summed over images */
   int64_t stage_victims[ORC_MAX_STAGES];
   int64_t stage_merges[ORC_MAX_STAGES];
+  uint8_t *victim_out;      /* optional [B][M]: the O6/O6' victim flags at the stop point (test export) */
 } orc_debug;
 
 #define ORC_OK 0

@@ -103,6 +103,7 @@ struct rapid_ctx {
   int sweep_gpw = 2;  // K4 word groups per warp (RAPID_SWEEP_GPW overrides, A/B testing)
   bool fuse_snap = false;  // RAPID_FUSE_SNAP=1: K3 of the next phase runs at the end of a cooperative K5 (measured: same step time)
   bool bset_parent = true;  // dyadic stages: boundary sets from the parent map (RAPID_BSET_PARENT=0: child-map tile pass)
+  bool no_smallb = false;   // RAPID_SWEEP_NO_SMALLB=1: every block stage takes K4's 64-bit position-factor variant (parity-tested variant)
   bool fuse_bset = false;  // RAPID_FUSE_BSET=1: dyadic transitions also write the next stage's boundary sets (measured: no faster than the separate pass)
   bool use_bset = true;  // RAPID_SWEEP=scan selects the full-scan path K4a + K4b (A/B testing)
   // CUDA graph of the whole segmentation (one launch per call): captured on a private stream,
@@ -330,7 +331,7 @@ int build_plan(rapid_ctx *c, int H, int W, const rapid_params *p) {
     int64_t mw = 0, mh = 0;
     for (int i = 0; i < S.nbx; i++) mw = std::max<int64_t>(mw, S.xs[i + 1] - S.xs[i]);
     for (int j = 0; j < S.nby; j++) mh = std::max<int64_t>(mh, S.ys[j + 1] - S.ys[j]);
-    S.smallb = S.b > 1 && mw * mh * (int64_t)(std::max(H, W) - 1) < (int64_t(1) << 22);
+    S.smallb = !c->no_smallb && S.b > 1 && mw * mh * (int64_t)(std::max(H, W) - 1) < (int64_t(1) << 22);
   }
   for (int s = 0; s < nst; s++) {
     StagePlan &S = N.st[s];
@@ -898,6 +899,7 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   if (const char *e = getenv("RAPID_FUSE_BSET")) c->fuse_bset = e[0] == '1';
   if (const char *e = getenv("RAPID_BSET_PARENT")) c->bset_parent = e[0] != '0';
   if (const char *e = getenv("RAPID_FUSE_SNAP")) c->fuse_snap = e[0] == '1';
+  if (const char *e = getenv("RAPID_SWEEP_NO_SMALLB")) c->no_smallb = e[0] == '1';
   c->tiles_grid = c->sm_count * tiles_occupancy();
   {
     const char *e = getenv("RAPID_SWEEP");

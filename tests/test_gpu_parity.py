@@ -186,8 +186,13 @@ def test_random_all_options_combined(rapid):
     """Random small cases over every option at once (size mode, mask rule, y model, stats
     mode, lambdas, stage lists, final grain, batches), each bit-exact with the oracle."""
     import os
-    rng = np.random.default_rng(int(os.environ.get("RAPID_RANDOM_SEED", "2024")))
-    for case in range(int(os.environ.get("RAPID_RANDOM_CASES", "24"))):
+    random_all_options(rapid, int(os.environ.get("RAPID_RANDOM_SEED", "2024")),
+                       int(os.environ.get("RAPID_RANDOM_CASES", "24")))
+
+
+def random_all_options(rapid, seed, n):
+    rng = np.random.default_rng(seed)
+    for case in range(n):
         B = int(rng.integers(1, 4))
         H, W = int(rng.integers(24, 140)), int(rng.integers(24, 140))
         imgs = np.stack([synth.image(H, W, int(rng.integers(1 << 30)), int(rng.integers(2, 12)),
@@ -214,3 +219,65 @@ def test_random_all_options_combined(rapid):
             assert_parity(rapid, imgs, p)
         except AssertionError as e:
             raise AssertionError(f"case {case}: B={B} H={H} W={W} params={p}: {e}") from None
+
+
+# ----------------------------------------------------------------------- hand-worked H2-H4, ties
+# (expected outputs worked out by hand in tests/test_oracle_choice.py; here the CUDA path must
+#  give the same maps, sums and counters as the oracle and the hand-worked result)
+def test_eq3_exact_ties_on_gpu(rapid):
+    from test_oracle_choice import _two_by_two
+    for colours, corner, want in [((100, 200, 200, 200), (3, 3), 1), ((200, 100, 200, 200), (4, 3), 0)]:
+        img = _two_by_two(colours, corner, 200)
+        o, lab, sp, info = assert_parity(rapid, img, P(4, [1], 1, lam_pos=0, lam_b=32 * 65536))
+        exp = np.repeat(np.repeat(np.array([[0, 1], [2, 3]], np.int32), 4, 0), 4, 1)
+        exp[corner[1], corner[0]] = want
+        assert np.array_equal(lab[0], exp)
+
+
+def test_H2_bridge_on_gpu(rapid):
+    from test_oracle_choice import _h2_image
+    o, lab, sp, info = assert_parity(rapid, _h2_image(), P(2, [1], 2, lam_pos=65536, lam_b=32 * 65536))
+    want = np.ones((6, 6), dtype=np.int32)
+    want[0, 0:3] = want[5, 0:3] = 0
+    want[1:5, 0] = 0
+    assert np.array_equal(lab[0], want)
+
+
+@pytest.mark.parametrize("mode,u,mid,T", [(0, (3, 2), 200, None), (1, (3, 2), 200, None), (2, (3, 2), 200, None),
+                                         (2, (7, 4), 200, 0), (2, (7, 4), 150, 2)])
+def test_H3_size_modes_on_gpu(rapid, mode, u, mid, T):
+    from test_oracle_choice import _h3_image, H3_HARD
+    p = P(3, [2], 2, lam_pos=0, lam_b=65536, size_mode=mode, l=(1, 2), u=u)
+    o, lab, sp, info = assert_parity(rapid, _h3_image(mid), p)
+    if mode == 0:
+        want = np.array([[0, 0, 0, 2, 2, 2], [0, 0, 0, 1, 2, 2]], np.int32)
+    else:
+        want = H3_HARD if T is None else np.where(H3_HARD == 1, T, H3_HARD)
+    assert np.array_equal(lab[0][::2, ::2], want)
+    assert list(info.stage_merges)[0] == (0 if T is None else 1)
+
+
+@pytest.mark.parametrize("rule", [1, 2, 3])
+def test_H4_gating_on_gpu(rapid, rule):
+    img = np.zeros((8, 8, 3), dtype=np.uint8)
+    img[:, 3:, :] = 200
+    p = P(2, [2, 1], 2, mask=rule, tau2=100)
+    p.protos = [(200, 200, 200)]
+    o, lab, sp, info = assert_parity(rapid, img, p)
+    want = np.zeros((8, 8), dtype=np.int32)
+    want[:, 4 if rule == 1 else 3:] = 1
+    assert np.array_equal(lab[0], want)
+    assert sp["y"].tolist() == [-1, 1]
+
+
+# ----------------------------------------------------------------------- 64-bit K4 variant
+def test_config4_strip_reaches_64bit_block_stage(rapid):
+    """A 128 x 32768 strip with config 4's densities, prediction and merges: at the b = 16 stage
+    (max block area) x (max coordinate) = 256 x 32767 >= 2^22, so K4 runs its 64-bit
+    position-factor variant (as config 4 itself does at b = 16) with real moves; labels, int64
+    sums, flags and per-phase counters bit-exact with the oracle."""
+    w = synth.scaled(4, 128, 32768)
+    assert 16 * 16 * (32768 - 1) >= 1 << 22
+    o, lab, sp, info = assert_parity(rapid, w.images(), w.params)
+    s16 = w.params.block_sizes.index(16)
+    assert o.counters[s16, ..., oracle.C_COMMIT].sum() > 100  # the 64-bit stage really moves blocks

@@ -31,7 +31,7 @@ def make_ctx(env, pixels, sps):
 
 
 VARIANTS = [{}, {"RAPID_NO_GRAPH": "1"}, {"RAPID_SWEEP": "scan"}, {"RAPID_FUSE_BSET": "1"}, {"RAPID_FUSE_SNAP": "1"},
-            {"RAPID_NO_TMA": "1"}, {"RAPID_BSET_PARENT": "0"}]
+            {"RAPID_NO_TMA": "1"}, {"RAPID_BSET_PARENT": "0"}, {"RAPID_SWEEP_NO_SMALLB": "1"}]
 
 
 @pytest.mark.parametrize("cfg,side", [(2, 1024), (4, 1024), (5, 0)])
@@ -208,3 +208,14 @@ def test_literal_pyramid_mode_oracle_exact(cfg, side):
     for f in ("n", "sum_r", "sum_g", "sum_b", "sum_x", "sum_y"):
         assert np.array_equal(sp[f], ref.sp[f]), f
     assert np.array_equal(info.counters()[..., oracle.C_COMMIT], ref.counters[..., oracle.C_COMMIT])
+
+
+def test_random_cases_through_64bit_block_variant():
+    """The randomized all-options sweep again with every block stage forced onto K4's 64-bit
+    position-factor variant (RAPID_SWEEP_NO_SMALLB=1): bit-exact with the oracle."""
+    from test_gpu_parity import random_all_options
+    r = make_ctx({"RAPID_SWEEP_NO_SMALLB": "1"}, 1 << 22, 1 << 16)
+    try:
+        random_all_options(r, 77, 16)
+    finally:
+        r.close()

@@ -151,3 +151,42 @@ def test_config4_sampled_block_decisions_match_oracle(cfg4):
         assert int(after[y, x]) == want, (y, x, code, A, B)
         moved += want != A
     assert moved >= 4000
+
+
+def test_config4_full_size_bit_exact_with_oracle(cfg4):
+    """North-star target #1 at the headline size: the whole config-4 segmentation (1.07 Gpx,
+    M = 2^20, MERGE + CLASS + REUSE, stages 32..1 incl. the 64-bit b = 16 stage) on the GPU, in
+    the launch configuration bench.py times (CUDA-graph replay), against the single-threaded
+    CPU oracle on the same input: labels, int64 sums, flags and every per-phase counter
+    element by element (oracle ~2-3 min and ~30 GB of host RAM)."""
+    import time
+    import torch
+    from gpu_util import CMP_FIELDS
+    w, host, img, r = cfg4
+    p = w.params
+    M = p.n_superpixels
+    labels = torch.empty((1, w.H, w.W), dtype=torch.int32, device="cuda")
+    r.segment(img, p, labels)  # capture
+    r.segment(img, p, labels)  # replay (the timed launch configuration)
+    torch.cuda.synchronize()
+    sp, info = r.stats(M)
+    g_lab = labels.cpu().numpy()
+    del labels
+    torch.cuda.empty_cache()
+    t0 = time.perf_counter()
+    o = oracle.segment(host.numpy(), p)
+    dt = time.perf_counter() - t0
+    print(f"\nconfig 4 oracle: {dt:.1f} s ({w.pixels / dt / 1e6:.2f} Mpx/s, 1 thread)")
+    diff = int((g_lab != o.labels).sum())
+    assert diff == 0, f"{diff} labels differ"
+    for f in CMP_FIELDS + ("y",):
+        assert np.array_equal(sp[f].astype(np.int64), o.sp[f].astype(np.int64)), f
+    alive = o.sp["alive"] == 1
+    assert np.array_equal(sp["active"][alive], o.sp["active"][alive]), "active"
+    gc, oc = info.counters(), o.counters
+    for s in range(len(p.block_sizes)):
+        run = int(info.stage_sweeps_run[s])
+        assert np.array_equal(gc[s, :run], oc[s, :run]), f"per-phase counters, stage {s}"
+    assert list(info.stage_merges)[:6] == o.stage_merges[:6]
+    assert list(info.stage_victims)[:6] == o.stage_victims[:6]
+    assert o.counters[1, ..., oracle.C_COMMIT].sum() > 10000  # the 64-bit b = 16 stage moves blocks

@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--setting", default="rapid", choices=list(synth.SETTINGS),
                     help="SURVEY f1 comparison setting (rapid = the headline workload)")
-    ap.add_argument("--sample", type=int, default=8192, help="side of the bounded CPU sample (~7 s of oracle work)")
+    ap.add_argument("--sample", type=int, default=8192, help="the bounded CPU sample is side x 2 side px (~15 s of oracle work at 8192)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-quality", action="store_true", help="skip the untimed f4 UE/BR report")
@@ -80,6 +80,19 @@ def max_over_ranks(x: float) -> float:
     return float(t.item())
 
 
+def kernel_sources_sha16():
+    """Hash of the CUDA sources (csrc/*.cu, *.cuh): ties a committed ncu traffic capture to the
+    kernels it measured."""
+    import hashlib
+    d = os.path.join(ROOT, "paper_1704_02083_b200", "csrc")
+    h = hashlib.sha256()
+    for n in sorted(os.listdir(d)):
+        if n.endswith((".cu", ".cuh")):
+            with open(os.path.join(d, n), "rb") as f:
+                h.update(n.encode() + b"\0" + f.read())
+    return h.hexdigest()[:16]
+
+
 def peaks():
     try:
         with open(MEASURED) as f:
@@ -107,7 +120,9 @@ def config_dict(w, extra=None):
 # ----------------------------------------------------------------------------- CPU oracle
 def oracle_sample(cfg, side, seed_offset=0, setting="rapid"):
     import oracle
-    sw = synth.with_setting(synth.scaled(cfg, side, side, seed_offset=seed_offset), setting)
+    base = synth.config(cfg)
+    H, W = min(side, base.H), min(2 * side, base.W)  # side x 2 side: ~15 s of oracle work at 8192
+    sw = synth.with_setting(synth.scaled(cfg, H, W, seed_offset=seed_offset), setting)
     img = sw.images()
     t0 = time.perf_counter()
     oracle.segment(img, sw.params)
@@ -115,11 +130,56 @@ def oracle_sample(cfg, side, seed_offset=0, setting="rapid"):
     return sw, dt
 
 
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
+class pinned_to_one_core:
+    """Run the (single-threaded) oracle pinned to one host core, as `taskset -c <core>` would
+    (BASELINE.md's CPU plan); the previous affinity is restored afterwards."""
+
+    def __enter__(self):
+        self.old = os.sched_getaffinity(0)
+        self.core = min(self.old)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.old)
+
+
+def full_oracle_record(cfg):
+    """The whole-workload oracle time measured once per round on the GPU box (tools/oracle_full.py
+    or the full-size parity test, same single-threaded C oracle, pinned to one core); reported
+    next to the live bounded sample, never in place of it."""
+    path = os.path.join(ROOT, "profiles", f"oracle_full_cfg{cfg}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f)
+
+
 def cpu_baseline(cfg, side, setting="rapid"):
-    sw, dt = oracle_sample(cfg, side, setting=setting)
-    return {"value": round(sw.pixels / dt / 1e6, 4), "unit": "Mpixel/s", "cores": 1, "kind": "oracle",
-            "sample": f"{sw.name}: {side}x{side} px with config {cfg}'s densities and parameters, "
-                      f"full pipeline, single-threaded C oracle, {dt:.2f} s"}
+    model, ncores = cpu_info()
+    with pinned_to_one_core() as pin:
+        sw, dt = oracle_sample(cfg, side, setting=setting)
+    out = {"value": round(sw.pixels / dt / 1e6, 4), "unit": "Mpixel/s", "cores": 1, "kind": "oracle",
+           "sample": f"{sw.name}: {sw.H}x{sw.W} px with config {cfg}'s densities and parameters, "
+                     f"full pipeline, single-threaded C oracle pinned to core {pin.core}, {dt:.2f} s",
+           "cpu_model": model, "host_cores": f"1 of {ncores}"}
+    full = full_oracle_record(cfg)
+    if full is not None and setting == "rapid":
+        out["full_workload"] = full
+    return out
 
 
 def run_reference(args):
@@ -128,10 +188,13 @@ def run_reference(args):
         return 0
     w = synth.with_setting(synth.config(args.config), args.setting)
     times = []
-    for i in range(args.warmup + args.steps):
-        sw, dt = oracle_sample(args.config, args.sample, seed_offset=0, setting=args.setting)
-        if i >= args.warmup:
-            times.append(dt)
+    side = max(1, args.sample // 2)  # side x 2 side per step: ~4 s of oracle work at config 4
+    model, ncores = cpu_info()
+    with pinned_to_one_core() as pin:
+        for i in range(args.warmup + args.steps):
+            sw, dt = oracle_sample(args.config, side, seed_offset=0, setting=args.setting)
+            if i >= args.warmup:
+                times.append(dt)
     px = sw.pixels
     tot = sum(times)
     value = px * len(times) / tot / 1e6
@@ -139,10 +202,12 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(tot / len(times) * 1e3, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": config_dict(w, {"reference_sample": f"{args.sample}x{args.sample} per step"}),
+            "config": config_dict(w, {"reference_sample": f"{sw.H}x{sw.W} per step"}),
             "cpu_baseline": {"value": round(value, 4), "unit": "Mpixel/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{args.sample}x{args.sample} px of config {args.config}'s "
-                                       "workload (same densities/params) per step, single-threaded C oracle"},
+                             "sample": f"{sw.H}x{sw.W} px of config {args.config}'s workload (same "
+                                       f"densities/params) per step, single-threaded C oracle pinned to "
+                                       f"core {pin.core}",
+                             "cpu_model": model, "host_cores": f"1 of {ncores}"},
             "e2e": {"value": round(value, 4), "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -334,15 +399,37 @@ def run_ours(args):
         steps_ms = float(prof_ms[[rb.K_PYRAMID, rb.K_SNAPSHOT, rb.K_PROPOSE, rb.K_COMMIT, rb.K_MERGE, rb.K_PREDICT,
                                   rb.K_TRANSITION, rb.K_FINAL, rb.K_EVAL]].sum())
         achieved = sweep_bytes / (sweep_ms / 1e3) / 1e9 if sweep_ms > 0 else 0.0
-        traffic = None
+        traffic, traffic_note = None, "no ncu capture committed"
         tfile = os.path.join(ROOT, "profiles", "sweep_traffic.json")
-        if os.path.exists(tfile):  # ncu dram bytes of one pixel-stage k_sweep launch (committed capture)
+        if os.path.exists(tfile):  # ncu dram bytes of the pixel-stage k_sweep launches (committed capture)
             with open(tfile) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                tj = json.load(f)
+            if tj.get("kernel_sources_sha16") == kernel_sources_sha16():
+                traffic = tj.get("dram_bytes_per_launch")
+                traffic_note = f"ncu capture of these kernel sources ({tj.get('source')})"
+            else:
+                traffic_note = "stale: the committed ncu capture predates the current kernel sources"
         all_bytes = sum(v[0] for v in pb.values())
         phase_ms = float(prof_ms[rb.K_PHASESET].sum())
+        # per stage: K4 alone and the per-phase set, bytes per the same model
+        per_stage = []
+        for st, b in enumerate(p.block_sizes):
+            runs_s = int(info.stage_sweeps_run[st]) * 4
+            cs = 3 if b == 1 else 8
+            topo_s = int(cnt[st, :, :, rb.C_TOPO].sum())
+            k4_bytes = 4 * window[st] * runs_s + cs * topo_s
+            k4_ms = float(prof_ms[rb.K_PROPOSE][st])
+            set_ms = float(prof_ms[rb.K_PHASESET][st])
+            per_stage.append({
+                "b": b, "phases": runs_s, "window_blocks": window[st],
+                "k4_ms": round(k4_ms, 3), "k4_GB": round(k4_bytes / 1e9, 4),
+                "k4_frac": round(k4_bytes / (k4_ms / 1e3) / 1e9 / peak, 4) if k4_ms > 0 else None,
+                "k3_ms": round(float(prof_ms[rb.K_SNAPSHOT][st]), 3), "k5_ms": round(float(prof_ms[rb.K_COMMIT][st]), 3),
+                "set_ms": round(set_ms, 3), "set_GB": round(pb[st][0] / 1e9, 4),
+                "set_frac": round(pb[st][0] / (set_ms / 1e3) / 1e9 / peak, 4) if set_ms > 0 else None})
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_note,
+                "phase_set_frac": round(all_bytes / (phase_ms / 1e3) / 1e9 / peak, 4) if phase_ms > 0 else None,
                 "kernel": f"k_sweep (K4: boundary-set driven scan + evaluate), pixel stage ({sweep_launch} launches/step)",
                 "bytes_per_launch": round(sweep_bytes / max(1, sweep_launch)),
                 "avg_launch_ms": round(sweep_ms / max(1, sweep_launch), 4),
@@ -353,7 +440,8 @@ def run_ours(args):
                               "frac": round(all_bytes / (phase_ms / 1e3) / 1e9 / peak, 4) if phase_ms > 0 else None,
                               "ms_per_step": round(phase_ms, 3),
                               "kernels": "K3 snapshot + K4 sweep + K5 commit, all stages",
-                              "bytes_model": "4 B x window + c_s x topology-passing candidates + 4 B x commits"}}
+                              "bytes_model": "4 B x window + c_s x topology-passing candidates + 4 B x commits"},
+                "per_stage": per_stage}
         line = {"metric": METRIC, "value": round(value, 3), "unit": "Mpixel/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",

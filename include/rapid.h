@@ -94,6 +94,7 @@ typedef struct {
   uint32_t block_size[RAPID_MAX_STAGES]; /* descending, 1..64, each divides the previous;
                                             the last is the final grain (Table 1) */
   uint32_t sweeps;           /* parity sweeps per stage, 0..RAPID_MAX_SWEEPS (A5, A25) */
+  uint8_t pad0_[4];          /* explicit padding (ignored; zeroed in the graph-cache key) */
   int64_t lambda_pos_q16;    /* lambda_pos in Q16.16, 0..2^31-1 */
   int64_t lambda_b_q16;      /* lambda_b in Q16.16 per ordered pixel pair, 0..2^31-1 (A3) */
   uint32_t size_mode;        /* RAPID_SIZE_* */
@@ -102,7 +103,7 @@ typedef struct {
   uint32_t mask_rule;        /* RAPID_MASK_* */
   uint32_t n_proto;          /* 1..4 when mask_rule != OFF */
   uint8_t proto_rgb[RAPID_MAX_PROTO][3]; /* prototypes of h_theta (A21) */
-  uint8_t pad_[4];
+  uint8_t pad_[8];           /* explicit padding (ignored; zeroed in the graph-cache key) */
   int64_t tau2;              /* y=+1 iff min_k ||c - proto_k||^2 <= tau2 (Eq. 6; intensity^2) */
   uint32_t stats_mode;       /* RAPID_STATS_* */
   uint32_t y_model;          /* RAPID_Y_* */

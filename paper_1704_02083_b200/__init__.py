@@ -36,6 +36,7 @@ class rapid_params(ctypes.Structure):
         ("n_stages", ctypes.c_uint32),
         ("block_size", ctypes.c_uint32 * MAX_STAGES),
         ("sweeps", ctypes.c_uint32),
+        ("pad0_", ctypes.c_uint8 * 4),
         ("lambda_pos_q16", ctypes.c_int64),
         ("lambda_b_q16", ctypes.c_int64),
         ("size_mode", ctypes.c_uint32),
@@ -46,7 +47,7 @@ class rapid_params(ctypes.Structure):
         ("mask_rule", ctypes.c_uint32),
         ("n_proto", ctypes.c_uint32),
         ("proto_rgb", (ctypes.c_uint8 * 3) * MAX_PROTO),
-        ("pad_", ctypes.c_uint8 * 4),
+        ("pad_", ctypes.c_uint8 * 8),
         ("tau2", ctypes.c_int64),
         ("stats_mode", ctypes.c_uint32),
         ("y_model", ctypes.c_uint32),

@@ -691,8 +691,12 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           }
           if (gated_sz) {
             Timer t2(c, s, RAPID_K_COMMIT, st);
-            if (fused_snap) launch_commit_snap(pa, pixel, c->sm_count, s);
-            else launch_commit(pa, pixel, c->sm_count * 8, s);  // latency-bound gathers: full occupancy
+            if (fused_snap) {
+              const cudaError_t e = launch_commit_snap(pa, pixel, c->sm_count, s);
+              if (e != cudaSuccess) return fail(c, RAPID_E_CUDA, std::string("cooperative launch k_commit<SNAP>: ") + cudaGetErrorString(e));
+            } else {
+              launch_commit(pa, pixel, c->sm_count * 8, s);  // latency-bound gathers: full occupancy
+            }
             c->launches++;
           }
           if (stop_at(RAPID_STOP_PHASE, st, t, ph)) return RAPID_OK;
@@ -740,7 +744,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       ma.flag = ctl->mflag;
       ma.bset = c->use_bset ? (const uint32_t *)c->bset.p : nullptr;
       ma.stage_info = &ctl->stage_info[st][0];
-      launch_merge_round(ma, has_tmap[st] ? tmaps[st].b : nullptr, c->tiles_grid, grid_k, s, &c->launches);
+      const cudaError_t me = launch_merge_round(ma, has_tmap[st] ? tmaps[st].b : nullptr, c->tiles_grid, grid_k, s, &c->launches);
+      if (me != cudaSuccess) return fail(c, RAPID_E_CUDA, std::string("cooperative launch k_merge_match: ") + cudaGetErrorString(me));
     }
     if (stop_at(RAPID_STOP_AFTER_MERGE, st, 0, 0)) {
       remap_in_place(st);
@@ -946,6 +951,8 @@ int rapid_segment(rapid_ctx *c, const uint8_t *image, int32_t H, int32_t W, cons
     k.prof = c->prof;
     k.plan_gen = c->plan_gen;
     k.p = *p;
+    memset(k.p.pad0_, 0, sizeof k.p.pad0_);  // the explicit padding never selects a graph
+    memset(k.p.pad_, 0, sizeof k.p.pad_);
     rapid_ctx::GraphEntry *ent = nullptr;
     for (auto &g : c->gcache)
       if (memcmp(&k, &g.key, sizeof k) == 0) ent = &g;

@@ -1326,7 +1326,7 @@ void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s) {
   k_snapshot<<<g, 256, 0, s>>>(a);
 }
 
-void launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int grid, cudaStream_t s,
+cudaError_t launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int grid, cudaStream_t s,
                         int *nlaunch) {
   const int nchunks = (a.K + CHUNK - 1) / CHUNK;
   k_flag_count<<<nchunks, 256, 0, s>>>(a.sp.victim, a.K, a.chunk, a.victim_any);
@@ -1340,22 +1340,23 @@ void launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int gri
   k_merge_scan_deg<<<1, 1024, 0, s>>>(a);
   k_merge_fill<<<grid, 256, 0, s>>>(a);
   {
-    static int coop_grid = 0;
-    if (!coop_grid) {
-      int nbk = 0, dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbk, k_merge_match, 256, 0);
-      coop_grid = sms * std::max(1, std::min(nbk, 4));
-    }
+    // co-resident grid computed per call (device / context of this launch), launch checked
+    int nbk = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbk, k_merge_match, 256, 0);
+    if (e != cudaSuccess) return e;
+    const int coop_grid = sms * std::max(1, std::min(nbk, 4));
     MergeArgs aa = a;
     void *args[] = {&aa};
-    cudaLaunchCooperativeKernel((const void *)k_merge_match, coop_grid, 256, args, 0, s);
+    e = cudaLaunchCooperativeKernel((const void *)k_merge_match, coop_grid, 256, args, 0, s);
+    if (e != cudaSuccess) return e;
   }
   k_merge_apply<<<grid, 256, 0, s>>>(a);
   k_merge_cleanup<<<grid, 256, 0, s>>>(a);
   k_merge_done<<<1, 1, 0, s>>>(a);
   *nlaunch += 12;
+  return cudaSuccess;
 }
 
 void launch_predict(const PredictArgs &a, int grid, cudaStream_t s, int *nlaunch) {

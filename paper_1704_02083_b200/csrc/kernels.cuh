@@ -306,7 +306,7 @@ void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s);
 void launch_scan(const PhaseArgs &a, const void *tmap, int grid, cudaStream_t s);
 void launch_eval(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
 void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
-void launch_commit_snap(const PhaseArgs &a, bool pixel, int sm_count, cudaStream_t s);
+cudaError_t launch_commit_snap(const PhaseArgs &a, bool pixel, int sm_count, cudaStream_t s);
 // boundary-set sweep: K4 build (once per stage) and the fused bitset-driven sweep
 void launch_bset_build(const PhaseArgs &a, const void *tmap, int grid, cudaStream_t s);
 void launch_sweep(const PhaseArgs &a, bool pixel, bool smallb, int sm_count, cudaStream_t s);
@@ -317,7 +317,7 @@ constexpr int CAND_SLACK_PER_WARP = 64;  // chunked reservations: unused tail pe
 // encode a 3-D TMA descriptor {nbx, nby, B} of int32 with box {TX+4, TY+2, 1};
 // false when nbx*4 is not a multiple of 16 B (the LDG loader is used then)
 bool make_label_tmap(void *tmap64B, int32_t *base, int nbx, int nby, int B);
-void launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int grid, cudaStream_t s,
+cudaError_t launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int grid, cudaStream_t s,
                         int *nlaunch);
 bool launch_merge_adjacency_tma(const MergeArgs &a, const void *tmap, int grid, cudaStream_t s);
 int tiles_occupancy();

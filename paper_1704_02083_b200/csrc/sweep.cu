@@ -1217,13 +1217,14 @@ void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
 }
 
 // K5 + the next K3 in one cooperative launch (grid = every CTA that fits at once)
-void launch_commit_snap(const PhaseArgs &a, bool pixel, int sm_count, cudaStream_t s) {
+cudaError_t launch_commit_snap(const PhaseArgs &a, bool pixel, int sm_count, cudaStream_t s) {
   const void *fn = pixel ? (const void *)k_commit<true, true> : (const void *)k_commit<false, true>;
-  int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 256, 0);
+  int nb = 0;  // per call: the current device / context decides what fits co-resident
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 256, 0);
+  if (e != cudaSuccess) return e;
   PhaseArgs copy = a;
   void *args[] = {&copy};
-  cudaLaunchCooperativeKernel(fn, dim3(sm_count * std::max(nb, 1)), dim3(256), args, 0, s);
+  return cudaLaunchCooperativeKernel(fn, dim3(sm_count * std::max(nb, 1)), dim3(256), args, 0, s);
 }
 
 }  // namespace rapid

@@ -80,3 +80,12 @@ def test_param_validation_happens_before_launch(built):
     assert lib.rapid_segment(None, None, 8, 8, ctypes.byref(p), None, None) == -1
     assert lib.rapid_stats(None, None, 0, None) == -1
     assert rb.rapid_status_string(-6) == "RECOUNT integrity check failed"
+
+
+def test_params_struct_has_no_implicit_padding():
+    """Every byte of rapid_params belongs to a named field (the padding is explicit), so a
+    C caller that fills it field by field cannot leave junk bytes that the graph-cache key
+    would see."""
+    import paper_1704_02083_b200 as rb
+    total = sum(ctypes.sizeof(t) for _, t in rb.rapid_params._fields_)
+    assert total == ctypes.sizeof(rb.rapid_params)

@@ -219,3 +219,27 @@ def test_random_cases_through_64bit_block_variant():
         random_all_options(r, 77, 16)
     finally:
         r.close()
+
+
+def test_host_stream_long_run_drains_flag_ring():
+    """rapid_segment_host_stream over n = 70 > 64 images with RECOUNT integrity checks: the
+    pinned 64-entry error-flag ring is drained once mid-stream and the 6-entry tail at the end;
+    every output equals the oracle and the call reports no integrity failure."""
+    import torch
+    n = 70
+    ws = [synth.scaled(3, 64, 64, seed_offset=k) for k in range(n)]
+    p = copy.deepcopy(ws[0].params)
+    p.stats_mode = synth.STATS_RECOUNT
+    imgs, labs = [], []
+    for w in ws:
+        h = torch.empty((1, w.H, w.W, 3), dtype=torch.uint8).pin_memory()
+        w.images(out=h.numpy())
+        imgs.append(h.numpy())
+        labs.append(torch.empty((1, w.H, w.W), dtype=torch.int32).pin_memory().numpy())
+    r = make_ctx({}, ws[0].pixels, p.n_superpixels)
+    try:
+        r.segment_host_stream(imgs, p, labs)  # raises RapidError on an integrity failure
+    finally:
+        r.close()
+    for k in range(n):
+        assert np.array_equal(labs[k], oracle.segment(imgs[k], p).labels), f"image {k}"

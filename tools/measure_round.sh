@@ -25,7 +25,10 @@ for r in rows[1:]:
 rd = [v["dram__bytes_read.sum"] for v in per.values()]
 wr = [v["dram__bytes_write.sum"] for v in per.values()]
 n = len(rd)
+sys.path.insert(0, ".")
+from bench import kernel_sources_sha16
 json.dump({"kernel": "k_sweep<true,true,4> (K4), config 4 pixel stage, all %d launches of one segmentation" % n,
+           "kernel_sources_sha16": kernel_sources_sha16(),
            "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none (profiles/%s_sweep_dram.csv)" % sys.argv[2],
            "launches": n, "dram_bytes_read_mean": sum(rd) / n, "dram_bytes_write_mean": sum(wr) / n,
            "dram_bytes_per_launch": (sum(rd) + sum(wr)) / n,

@@ -635,7 +635,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       Timer tm(c, s, RAPID_K_PHASESET, st);
       {
         Timer t2(c, s, RAPID_K_SNAPSHOT, st);
-        SnapArgs sa{sp, K, 0u};
+        SnapArgs sa{sp, K, 0u, (long long)p->l_num, (long long)p->l_den};
         launch_snapshot(sa, grid_k, s);
         c->launches++;
       }
@@ -643,7 +643,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
         for (int ph = 0; ph < 4; ph++, g++) {
           if (!(t == 0 && ph == 0) && !fused_snap) {  // (fused: the previous commit refreshed them)
             Timer t2(c, s, RAPID_K_SNAPSHOT, st);
-            SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1)};
+            SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, (long long)p->l_den};
             launch_snapshot(sa, grid_k, s);
             c->launches++;
           }
@@ -706,7 +706,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     {  // snapshot of the last phase's changes (merge round / prediction read it)
       Timer t2(c, s, RAPID_K_SNAPSHOT, st);
       if (g > 0 && !fused_snap) {
-        SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1)};
+        SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, (long long)p->l_den};
         launch_snapshot(sa, grid_k, s);
         c->launches++;
       }
@@ -753,7 +753,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     }
     if (st == 0 && mask != RAPID_MASK_OFF) {
       Timer tm(c, s, RAPID_K_PREDICT, st);
-      SnapArgs sa{sp, K, 0u};
+      SnapArgs sa{sp, K, 0u, (long long)p->l_num, (long long)p->l_den};
       launch_snapshot(sa, grid_k, s);
       c->launches++;
       PredictArgs pr;
@@ -905,6 +905,7 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   if (const char *e = getenv("RAPID_BSET_PARENT")) c->bset_parent = e[0] != '0';
   if (const char *e = getenv("RAPID_FUSE_SNAP")) c->fuse_snap = e[0] == '1';
   if (const char *e = getenv("RAPID_SWEEP_NO_SMALLB")) c->no_smallb = e[0] == '1';
+  if (const char *e = getenv("RAPID_PDL")) g_pdl = e[0] == '1';
   c->tiles_grid = c->sm_count * tiles_occupancy();
   {
     const char *e = getenv("RAPID_SWEEP");

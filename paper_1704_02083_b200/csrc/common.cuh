@@ -85,7 +85,7 @@ struct SpDev {
   uint8_t *alive, *active;   // [K]
   int8_t *y;                 // [K]
   uint8_t *victim;           // [K]
-  int32_t *out;              // [K] proposed outflow of the current phase
+  int32_t *out;              // [K] rem: outflow budget left in the current phase (O6', A19)
   uint32_t *dirty;           // [K] stamp of the last dirty-list insertion
   int32_t *remap;            // [K]
 };
@@ -136,6 +136,14 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
 }
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Programmatic dependent launch (phase-loop kernels, RAPID_PDL): wait until the previous kernel
+// in the stream has completed and its writes are visible (a no-op without a PDL launch), then
+// let the next kernel's CTAs be launched while this one runs (they block in their own wait).
+__device__ __forceinline__ void pdl_wait_and_trigger() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // Warp-aggregated delta update of the six int64 sums of superpixel `key` (north star (d)):
 // __match_any_sync groups the lanes by key, every group is reduced at once with REDUX
@@ -317,7 +325,7 @@ __device__ __forceinline__ void agg_sums_small(bool valid, int key, const long l
   }
 }
 
-// Warp-aggregated int32 add (proposal outflow per source superpixel); v in [0, 2^16).
+// Warp-aggregated int32 add (proposal outflow per source superpixel); |v| < 2^16.
 __device__ __forceinline__ void agg_add_i32(bool valid, int key, int v, int32_t *arr) {
   if (__ballot_sync(FULL, valid) == 0u) return;  // warp-uniform
   const WarpRun run = warp_runs(valid, key);

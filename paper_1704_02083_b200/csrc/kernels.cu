@@ -232,6 +232,7 @@ __global__ void k_stats0(const InitArgs a) {
 
 // ------------------------------------------------------------------ K3: snapshot
 __global__ void __launch_bounds__(256, 8) k_snapshot(const SnapArgs a) {  // one wave at K = 2^20
+  pdl_wait_and_trigger();
   snapshot_warps(a, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5);
 }
 
@@ -1323,7 +1324,7 @@ void launch_stats0(const InitArgs &a, cudaStream_t s) {
 void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s) {
   // one pass: every warp checks 128 stamps once (grid capped at `grid` x 2)
   const int g = grid_for(((size_t)a.K + 127) / 128 * 32, 256, 2 * grid);
-  k_snapshot<<<g, 256, 0, s>>>(a);
+  launch_pdl(k_snapshot, dim3(g), dim3(256), s, a);
 }
 
 cudaError_t launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int grid, cudaStream_t s,

@@ -35,6 +35,7 @@ struct SnapArgs {
   SpDev sp;
   int32_t K;
   uint32_t stamp;             // 0: refresh all; else only superpixels with dirty == stamp
+  long long l_num, l_den;     // size floor l (the outflow budget rem[] of the next phase)
 };
 
 struct MergeArgs {
@@ -200,7 +201,7 @@ bool launch_pyramid_leaf24(const StageDev &st, const StageDev &up, const uint8_t
 void launch_init_map0(const InitArgs &a, cudaStream_t s);
 void launch_stats0(const InitArgs &a, cudaStream_t s);
 // ------------------------------------------------------------------ K3: snapshot (device side)
-__device__ __forceinline__ void make_rec(const SpDev &sp, int k) {
+__device__ __forceinline__ Rec make_rec(const SpDev &sp, int k) {
   // gathers with a 64-B L2 fill (ld64_*, common.cuh); coherent: the fused commit + snapshot
   // kernel reads sums its own atomics wrote
   const ulonglong2 s01 = ld64_v2u64(sp.sums + (size_t)k * SUMW), s23 = ld64_v2u64(sp.sums + (size_t)k * SUMW + 2);
@@ -246,6 +247,18 @@ __device__ __forceinline__ void make_rec(const SpDev &sp, int k) {
   r.cq2f = c2 | (flags << 16);
   r.pad0 = r.pad1 = 0;
   sp.rec[k] = r;
+  return r;
+}
+
+// O6' budget of the next phase (A19): A's proposals commit iff their total outflow o keeps
+// (n_snap - o) l_den >= l_num InitSize, i.e. o <= rem = floor((n_snap l_den - l_num InitSize) / l_den);
+// K4 subtracts each proposal from rem[A], so K5 accepts A's proposals iff rem[A] >= 0 after K4
+__device__ __forceinline__ int32_t outflow_budget(const Rec &r, long long l_num, long long l_den) {
+  if (l_den <= 0) return 0;
+  const long long S = (long long)r.n * l_den - l_num * (long long)r.init;
+  long long q = S / l_den;
+  if (q * l_den > S) q--;  // floor for negative S
+  return (int32_t)q;
 }
 
 // Full refresh (stamp 0) or only the superpixels stamped dirty by the previous phase, by warps
@@ -292,16 +305,34 @@ __device__ __forceinline__ void snapshot_warps(const SnapArgs &a, int wid, int n
         }
         bit = __ffs(mm) - 1;
         const int k = 4 * (ch * 32 + j) + bit;
-        make_rec(a.sp, k);
-        // the proposed outflow of the next phase starts at zero: every superpixel whose
-        // out[] the last phase raised (every proposal's source) was stamped dirty by K5
-        a.sp.out[k] = 0;
+        const Rec r = make_rec(a.sp, k);
+        // the outflow budget of the next phase starts full: every superpixel whose rem[] the
+        // last phase lowered (every proposal's source) was stamped dirty by K4 or K5
+        a.sp.out[k] = outflow_budget(r, a.l_num, a.l_den);
       }
     }
   }
 }
 
 void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s);
+
+// Launch with the programmatic-stream-serialization attribute when g_pdl is set (the kernel must
+// begin with pdl_wait_and_trigger()); a plain stream-ordered launch otherwise.
+extern bool g_pdl;
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cfg.attrs = g_pdl ? at : nullptr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
 // K4a: tmap = TMA descriptor of the stage map (CUtensorMap*), or null for the LDG loader
 void launch_scan(const PhaseArgs &a, const void *tmap, int grid, cudaStream_t s);
 void launch_eval(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);

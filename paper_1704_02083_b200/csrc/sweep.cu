@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(K4B_THREADS, K4B_MIN_BLOCKS) k_eval(const Phas
         agg_sums(prop, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp);
         agg_sums(prop, kb + Bm, d, false, a.sp.sums, a.sp.dirty, a.stamp);
         c_commit += __popc(pm);
-      } else {
-        agg_add_i32(prop, kb + A, (int)d[0], a.sp.out);
+      } else {  // outflow budget, as in k_sweep
+        agg_add_i32(prop, kb + A, -(int)d[0], a.sp.out);
         const int np = __popc(pm);
         if (np > pleft) {  // retire the rest of the chunk (sentinels), reserve a new one
           if (lane < pleft) a.props[pbase + lane] = make_uint4(0u, 0xffffffffu, 0u, 0u);
@@ -737,6 +737,7 @@ __device__ __forceinline__ i128 energy(const Rec &ra, const int4 rb, const int d
 // map (boundary, static gate, simple point, Eq. 7), then evaluates Eqs. 1-3 as K4b does.
 template <bool PIXEL, bool GATED, int MINB, bool SMALLB = false>
 __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) {
+  pdl_wait_and_trigger();
   if (sweep_skipped(a.prev)) return;
   const int lane = lane_id();
   const StageDev &st = a.st;
@@ -992,7 +993,9 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
           }
           if (lane == 0) atomicAdd(&s_cnt[4], __popc(pm));
         } else {
-          agg_add_i32(prop, kb + A, (int)d[0], a.sp.out);
+          // HARD / MERGE: A's outflow is subtracted from its budget rem[A]; K5 applies A's moves
+          // iff rem[A] >= 0 afterwards (all-or-nothing, A19)
+          agg_add_i32(prop, kb + A, -(int)d[0], a.sp.out);
           const int np = __popc(pm);
           if (np > pleft) {  // retire the rest of the chunk (sentinels), reserve a new one
             if (lane < pleft) a.props[pbase + lane] = make_uint4(0u, 0xffffffffu, 0u, 0u);
@@ -1019,10 +1022,15 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
 }
 
 // ------------------------------------------------------------------ K5: commit
+// O6' (A19): the proposals of source A commit iff A's total outflow fits its budget, i.e. iff
+// rem[A] >= 0 after K4 subtracted every proposal of A (all-or-nothing; one 4-B gather from the
+// small budget table per proposal).  Accepted moves are applied here: label, boundary-set bits,
+// warp-aggregated sums; a rejected source is stamped dirty (its budget is restored next phase).
 // SNAP (cooperative launch, every CTA resident): after a grid barrier the same CTAs refresh the
-// records this commit stamped dirty (K3 of the next phase / of the stage end, without a launch)
+// records stamped dirty in this phase (K3 of the next phase / of the stage end, without a launch)
 template <bool PIXEL, bool SNAP>
 __global__ void __launch_bounds__(256, 8) k_commit(const PhaseArgs a) {  // 8 CTAs/SM: the grid is one wave
+  pdl_wait_and_trigger();
   const unsigned long long n = cta_count(a.prev, a.prop_count, !SNAP);
   if (n == 0) return;  // SNAP: grid-uniform (an empty list stamps nothing to refresh)
   unsigned c_commit = 0, c_rej = 0;
@@ -1034,31 +1042,27 @@ __global__ void __launch_bounds__(256, 8) k_commit(const PhaseArgs a) {  // 8 CT
     long long d[6] = {0, 0, 0, 0, 0, 0};
     const uint4 pr = valid ? a.props[i] : make_uint4(0u, 0xffffffffu, 0u, 0u);
     if (pr.y != 0xffffffffu) {  // skip unused reserved slots
-      const size_t idx = pr.x;
       A = (int)pr.y;
       B = (int)pr.z;
       const int img = (int)fdivu(pr.x, a.st.fd_nper);
       const uint32_t r = pr.x - (uint32_t)img * a.st.fd_nper.d;
       const int gy = (int)fdivu(r, a.st.fd_nbx), gx = (int)(r - (uint32_t)gy * (uint32_t)a.st.nbx);
       kb = img * a.M;
-      // the block's data (loads at block stages) is issued with the record and outflow loads
+      // the block's data (loads at block stages) is issued with the budget load
       if (PIXEL) {
         d[0] = 1; d[1] = pr.w & 0xffu; d[2] = (pr.w >> 8) & 0xffu; d[3] = (pr.w >> 16) & 0xffu;
         d[4] = gx; d[5] = gy;
       } else {
         block_data_blk(a.st, img, gx, gy, d);
       }
-      const int4 rb = ldnc64_v4(reinterpret_cast<const int4 *>(&a.sp.rec[kb + A]) + 1);  // n, init
-      const int outA = (int)ldnc64_u32(&a.sp.out[kb + A]);
-      // O6' all-or-nothing budget: the total proposed outflow must keep A >= l * InitSize (A19)
-      ok = !(((long long)rb.x - (long long)outA) * a.l_den < a.l_num * (long long)rb.y);
+      ok = (int)ldnc64_u32(&a.sp.out[kb + A]) >= 0;
       if (ok) {
-        a.st.map[idx] = B;
+        a.st.map[pr.x] = B;
         if (a.bset) bset_insert(a.bset, a.st, img, gx, gy, pr.w >> 24);
       } else {
         rej = true;
         for (int f = 0; f < 6; f++) d[f] = 0;
-        a.sp.dirty[kb + A] = a.stamp;  // so that the next K3 resets out[A] (and re-derives A's record)
+        a.sp.dirty[kb + A] = a.stamp;  // so that the next K3 restores rem[A] (and re-derives A's record)
         if (a.size_mode == 2) {
           a.sp.victim[kb + A] = 1;
           *a.victim_any = 1u;
@@ -1081,7 +1085,7 @@ __global__ void __launch_bounds__(256, 8) k_commit(const PhaseArgs a) {  // 8 CT
   }
   if (SNAP) {  // n is grid-uniform (cta_count per_cta = false): every CTA gets here or none did
     cg::this_grid().sync();
-    const SnapArgs sa{a.sp, a.B * a.M, a.stamp};
+    const SnapArgs sa{a.sp, a.B * a.M, a.stamp, a.l_num, a.l_den};
     snapshot_warps(sa, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5);
   }
 }
@@ -1147,6 +1151,7 @@ void launch_eval(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
 // registers), the block stages at 3 (80; their 64-bit position sums spill at 64).
 // RAPID_SWEEP_MINB=2..4 forces one budget for every stage (A/B testing).
 static int g_sweep_minb = 0;
+bool g_pdl = false;  // RAPID_PDL=1: programmatic dependent launch of the phase-loop kernels
 static int g_sweep_minb_small = 4;  // RAPID_SWEEP_MINB_SMALL: CTAs/SM of the small-block variant (4: 64 registers, a few bytes of spill, -0.1 ms)
 
 template <int MB>
@@ -1198,13 +1203,13 @@ void launch_sweep(const PhaseArgs &a, bool pixel, bool smallb, int sm_count, cud
   const int mb = g_sweep_minb ? g_sweep_minb : (pixel ? 4 : smallb ? g_sweep_minb_small : 3);
   if (!occ[mb]) occ[mb] = mb == 2 ? sweep_occ<2>() : mb == 3 ? sweep_occ<3>() : sweep_occ<4>();
   const int grid = sm_count * occ[mb];
-#define RAPID_SWEEP_LAUNCH(MB)                                                         \
-  if (pixel && gated) k_sweep<true, true, MB><<<grid, K4B_THREADS, 0, s>>>(a);         \
-  else if (pixel) k_sweep<true, false, MB><<<grid, K4B_THREADS, 0, s>>>(a);            \
-  else if (gated && smallb) k_sweep<false, true, MB, true><<<grid, K4B_THREADS, 0, s>>>(a); \
-  else if (smallb) k_sweep<false, false, MB, true><<<grid, K4B_THREADS, 0, s>>>(a);    \
-  else if (gated) k_sweep<false, true, MB><<<grid, K4B_THREADS, 0, s>>>(a);            \
-  else k_sweep<false, false, MB><<<grid, K4B_THREADS, 0, s>>>(a);
+#define RAPID_SWEEP_LAUNCH(MB)                                                                     \
+  if (pixel && gated) launch_pdl(k_sweep<true, true, MB>, dim3(grid), dim3(K4B_THREADS), s, a);        \
+  else if (pixel) launch_pdl(k_sweep<true, false, MB>, dim3(grid), dim3(K4B_THREADS), s, a);           \
+  else if (gated && smallb) launch_pdl(k_sweep<false, true, MB, true>, dim3(grid), dim3(K4B_THREADS), s, a); \
+  else if (smallb) launch_pdl(k_sweep<false, false, MB, true>, dim3(grid), dim3(K4B_THREADS), s, a);   \
+  else if (gated) launch_pdl(k_sweep<false, true, MB>, dim3(grid), dim3(K4B_THREADS), s, a);           \
+  else launch_pdl(k_sweep<false, false, MB>, dim3(grid), dim3(K4B_THREADS), s, a);
   if (mb == 2) { RAPID_SWEEP_LAUNCH(2) }
   else if (mb == 4) { RAPID_SWEEP_LAUNCH(4) }
   else { RAPID_SWEEP_LAUNCH(3) }
@@ -1212,8 +1217,8 @@ void launch_sweep(const PhaseArgs &a, bool pixel, bool smallb, int sm_count, cud
 }
 
 void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
-  if (pixel) k_commit<true, false><<<grid, 256, 0, s>>>(a);
-  else k_commit<false, false><<<grid, 256, 0, s>>>(a);
+  if (pixel) launch_pdl(k_commit<true, false>, dim3(grid), dim3(256), s, a);
+  else launch_pdl(k_commit<false, false>, dim3(grid), dim3(256), s, a);
 }
 
 // K5 + the next K3 in one cooperative launch (grid = every CTA that fits at once)

@@ -502,8 +502,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
   c->stopped = false;
   c->stop_map = nullptr;
   cudaMemsetAsync(ctl, 0, sizeof(Ctl), s);
-  // dirty stamps restart every call (stamps are call-invariant, so a captured graph replays)
-  cudaMemsetAsync(c->dirty, 0, sizeof(uint32_t) * K, s);
+  // the dirty bitmap starts empty every call (a captured graph replays)
+  cudaMemsetAsync(c->dirty, 0, sizeof(uint32_t) * ((K + 31) / 32 + 1), s);
 
   StageDev sd[MAXS];
   struct alignas(64) TMap {
@@ -643,7 +643,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
         for (int ph = 0; ph < 4; ph++, g++) {
           if (!(t == 0 && ph == 0) && !fused_snap) {  // (fused: the previous commit refreshed them)
             Timer t2(c, s, RAPID_K_SNAPSHOT, st);
-            SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, (long long)p->l_den};
+            SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, (long long)p->l_den,
+                        t > 0 ? &ctl->cnt[st][t - 1][0][0] : nullptr};
             launch_snapshot(sa, grid_k, s);
             c->launches++;
           }
@@ -695,7 +696,11 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
               const cudaError_t e = launch_commit_snap(pa, pixel, c->sm_count, s);
               if (e != cudaSuccess) return fail(c, RAPID_E_CUDA, std::string("cooperative launch k_commit<SNAP>: ") + cudaGetErrorString(e));
             } else {
-              launch_commit(pa, pixel, c->sm_count * 8, s);  // latency-bound gathers: full occupancy
+              // latency-bound gathers: up to full occupancy, but no more CTAs than ~4 proposals
+              // each at most (a phase proposes at most a quarter of the stage's blocks)
+              const long long maxp = ((long long)B * sd[st].nbx * sd[st].nby + 3) / 4;
+              const int cgrid = (int)std::min<long long>(c->sm_count * 8, std::max<long long>(c->sm_count, (maxp + 1023) / 1024));
+              launch_commit(pa, pixel, cgrid, s);
             }
             c->launches++;
           }
@@ -706,7 +711,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     {  // snapshot of the last phase's changes (merge round / prediction read it)
       Timer t2(c, s, RAPID_K_SNAPSHOT, st);
       if (g > 0 && !fused_snap) {
-        SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, (long long)p->l_den};
+        SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, (long long)p->l_den,
+                    sweeps > 0 ? &ctl->cnt[st][sweeps - 1][0][0] : nullptr};
         launch_snapshot(sa, grid_k, s);
         c->launches++;
       }

@@ -86,7 +86,7 @@ struct SpDev {
   int8_t *y;                 // [K]
   uint8_t *victim;           // [K]
   int32_t *out;              // [K] rem: outflow budget left in the current phase (O6', A19)
-  uint32_t *dirty;           // [K] stamp of the last dirty-list insertion
+  uint32_t *dirty;           // [(K + 31) / 32] bitmap: superpixels whose sums (or budget) changed this phase
   int32_t *remap;            // [K]
 };
 
@@ -245,6 +245,10 @@ __device__ __forceinline__ void red_add_keep(unsigned long long *p, unsigned lon
   asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
 }
 
+__device__ __forceinline__ void mark_dirty(uint32_t *dirty, int key) {
+  atomicOr(&dirty[key >> 5], 1u << (key & 31));
+}
+
 __device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[6], bool negate,
                                          unsigned long long *sums, uint32_t *dirty, uint32_t stamp) {
   if (__ballot_sync(FULL, valid) == 0u) return;  // warp-uniform
@@ -269,7 +273,7 @@ __device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[
     unsigned long long *s = sums + (size_t)key * SUMW;
 #pragma unroll
     for (int f = 0; f < 6; f++) red_add_keep(&s[f], (unsigned long long)(negate ? -tot[f] : tot[f]));
-    if (dirty != nullptr) dirty[key] = stamp;
+    if (dirty != nullptr) mark_dirty(dirty, key);
   }
 }
 
@@ -321,7 +325,7 @@ __device__ __forceinline__ void agg_sums_small(bool valid, int key, const long l
     unsigned long long *s = sums + (size_t)key * SUMW;
 #pragma unroll
     for (int f = 0; f < 6; f++) red_add_keep(&s[f], (unsigned long long)(negate ? -tot[f] : tot[f]));
-    if (dirty != nullptr) dirty[key] = stamp;
+    if (dirty != nullptr) mark_dirty(dirty, key);
   }
 }
 

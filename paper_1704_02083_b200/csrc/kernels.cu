@@ -233,6 +233,7 @@ __global__ void k_stats0(const InitArgs a) {
 // ------------------------------------------------------------------ K3: snapshot
 __global__ void __launch_bounds__(256, 8) k_snapshot(const SnapArgs a) {  // one wave at K = 2^20
   pdl_wait_and_trigger();
+  if (sweep_skipped(a.prev)) return;
   snapshot_warps(a, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5);
 }
 

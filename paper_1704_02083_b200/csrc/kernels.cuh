@@ -21,7 +21,7 @@ struct PhaseArgs {
   unsigned long long *cand_count;
   uint4 *props;              // proposals {stage-map index, A, B, packed RGB (pixel stage)}
   unsigned long long *prop_count;
-  uint32_t stamp;            // dirty stamp of this phase (superpixels whose sums change)
+  uint32_t stamp;            // phase index (non-zero)
   unsigned long long *cnt;        // [NCNT] counters of this phase
   const unsigned long long *prev; // counters of the previous sweep (phase 0), or null
   uint32_t *victim_any;
@@ -34,8 +34,10 @@ struct PhaseArgs {
 struct SnapArgs {
   SpDev sp;
   int32_t K;
-  uint32_t stamp;             // 0: refresh all; else only superpixels with dirty == stamp
+  uint32_t stamp;             // 0: refresh all; else only the superpixels marked in the dirty bitmap
   long long l_num, l_den;     // size floor l (the outflow budget rem[] of the next phase)
+  const unsigned long long *prev = nullptr;  // counters of the previous sweep: a skipped sweep (A25)
+                                             // changed nothing, so there is nothing to refresh
 };
 
 struct MergeArgs {
@@ -261,23 +263,29 @@ __device__ __forceinline__ int32_t outflow_budget(const Rec &r, long long l_num,
   return (int32_t)q;
 }
 
-// Full refresh (stamp 0) or only the superpixels stamped dirty by the previous phase, by warps
-// wid = 0 .. nw-1.  A warp takes 128 consecutive stamps (one 16-B load per lane; the array is
-// padded to a multiple of 4), compacts the dirty ones and refreshes them 32 at a time (one
-// record per lane).  Also run at the end of the commit kernel (after a grid barrier).
+// Full refresh (stamp 0) or only the superpixels marked in the dirty bitmap (one bit per
+// superpixel, set by the commits of the previous phase), by warps wid = 0 .. nw-1.  A warp takes
+// 128 consecutive superpixels (4 bitmap words; lane l looks at the 4-bit slice l of them and
+// clears the words it read), compacts the marked ones and refreshes them 32 at a time (one record
+// per lane).  Also run at the end of the commit kernel (after a grid barrier).
 __device__ __forceinline__ void snapshot_warps(const SnapArgs &a, int wid, int nw) {
   const int lane = lane_id();
   const int n4 = (a.K + 3) >> 2;
   const int nchunks = (n4 + 31) >> 5;
   for (int ch = wid; ch < nchunks; ch += nw) {
-    const int i = ch * 32 + lane;
+    const int i = ch * 32 + lane;  // 4-superpixel slice: superpixels 4i .. 4i+3
     unsigned m = 0;
     if (i < n4) {
-      const uint4 s4 = a.stamp ? *reinterpret_cast<const uint4 *>(a.sp.dirty + 4 * (size_t)i) : make_uint4(0, 0, 0, 0);
-      const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
+      uint32_t *wp = a.sp.dirty + (i >> 3);
+      const uint32_t wv = *wp;
+      if (a.stamp == 0u) {
 #pragma unroll
-      for (int j = 0; j < 4; j++)
-        if (4 * i + j < a.K && (a.stamp == 0u || sv[j] == a.stamp)) m |= 1u << j;
+        for (int j = 0; j < 4; j++)
+          if (4 * i + j < a.K) m |= 1u << j;
+      } else {
+        m = (wv >> (4 * (i & 7))) & 0xfu;
+      }
+      if ((lane & 7) == 0 && wv != 0u) *wp = 0u;  // every bit of the word is handled in this chunk
     }
     unsigned incl = __popc(m);
 #pragma unroll
@@ -307,7 +315,7 @@ __device__ __forceinline__ void snapshot_warps(const SnapArgs &a, int wid, int n
         const int k = 4 * (ch * 32 + j) + bit;
         const Rec r = make_rec(a.sp, k);
         // the outflow budget of the next phase starts full: every superpixel whose rem[] the
-        // last phase lowered (every proposal's source) was stamped dirty by K4 or K5
+        // last phase lowered (every proposal's source) was marked dirty by K4 or K5
         a.sp.out[k] = outflow_budget(r, a.l_num, a.l_den);
       }
     }

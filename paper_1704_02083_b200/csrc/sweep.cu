@@ -768,6 +768,7 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
   __syncthreads();
   unsigned long long pbase = 0;  // this warp's reserved proposal slots
   int pleft = 0;
+  unsigned r_cand = 0, r_topo = 0, r_prop = 0, r_srej = 0, r_commit = 0;  // this warp's counters
   // dynamic distribution of the word groups (one returned atomic per group and warp): the
   // per-group work varies with the boundary density, static striding left a 10 % tail
   for (unsigned g = 0;;) {
@@ -820,17 +821,25 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
         gx = (int)(pj & 0xffffu) + 2 * (int)bit;
         gy = (int)(pj >> 16);
         // block data depends on the position only: issued together with the window loads
-        uint64_t pk = 0;
-        int bx0 = 0, bx1 = 1, by0 = 0, by1 = 1;
+        // (kept raw until it is needed, so that no use of it waits before the window loads go out)
+        uint32_t pk32 = 0;
+        uint64_t pk64 = 0;
+        int bx0 = 0, bw = 1, by0 = 0, bh = 1;
         if (PIXEL) {
           const uint8_t *p = a.image + (((size_t)img * a.H + gy) * a.W + gx) * 3;
           rgb = ld_stream64(p) | (ld_stream64(p + 1) << 8) | (ld_stream64(p + 2) << 16);
         } else {
           const size_t bi = ((size_t)img * nby + gy) * nbx + gx;
-          pk = st.bsum32 ? widen_bsum32(ld_stream64(reinterpret_cast<const uint32_t *>(st.bsum) + bi))
-                         : ld_stream64(reinterpret_cast<const unsigned long long *>(st.bsum) + bi);
-          bx0 = st.xs[gx]; bx1 = st.xs[gx + 1];
-          by0 = st.ys[gy]; by1 = st.ys[gy + 1];
+          if (st.bsum32) pk32 = ld_stream64(reinterpret_cast<const uint32_t *>(st.bsum) + bi);
+          else pk64 = ld_stream64(reinterpret_cast<const unsigned long long *>(st.bsum) + bi);
+          if (st.uniform) {  // every block b x b at (gx b, gy b): no geometry-table loads
+            bx0 = gx * st.b;
+            by0 = gy * st.b;
+            bw = bh = st.b;
+          } else {
+            bx0 = st.xs[gx]; bw = st.xs[gx + 1] - bx0;
+            by0 = st.ys[gy]; bh = st.ys[gy + 1] - by0;
+          }
         }
         const int32_t *m = st.map + (size_t)img * nby * nbx;
         const size_t o = (size_t)gy * nbx + gx;
@@ -845,8 +854,6 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
         const int dNE = hN && hE ? RAPID_WLD(m + o - nbx + 1) : -1, dSE = hS && hE ? RAPID_WLD(m + o + nbx + 1) : -1;
         const int dSW = hS && hW ? RAPID_WLD(m + o + nbx - 1) : -1, dNW = hN && hW ? RAPID_WLD(m + o - nbx - 1) : -1;
         const int nq[4] = {nq0, nq1, nq2, nq3};
-        const bool bnd = (nq0 >= 0 && nq0 != A) | (nq1 >= 0 && nq1 != A) | (nq2 >= 0 && nq2 != A) |
-                         (nq3 >= 0 && nq3 != A);
         // topology (E_topo) and the distinct candidate labels need only the window; the
         // records of A and of the candidates are then loaded together (one dependent L2
         // round trip instead of two)
@@ -856,15 +863,17 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
                             ((unsigned)(dNW == A) << 7);
         const bool topo_ok = (s_simple[m8 >> 5] >> (m8 & 31u)) & 1u;
         // distinct candidate labels (A8), compacted: cb[0..nb) with the slot mask cm of each;
-        // maskA = slots labelled A.  Records: first 16 B (means + flags).
+        // maskA = slots labelled A.  (Compaction keeps the candidate loop below SIMD-coherent:
+        // every lane's first candidate is evaluated in the same iteration.)
+        const unsigned maskA = (m8 & 1u) | ((m8 >> 1) & 2u) | ((m8 >> 2) & 4u) | ((m8 >> 3) & 8u);
+        const bool bnd = (nq0 >= 0 && nq0 != A) | (nq1 >= 0 && nq1 != A) | (nq2 >= 0 && nq2 != A) |
+                         (nq3 >= 0 && nq3 != A);
         int cb[4] = {0, 0, 0, 0};
         unsigned cm[4] = {0u, 0u, 0u, 0u};
-        unsigned maskA = 0;
         int nb = 0;
 #pragma unroll
         for (int s = 0; s < 4; s++) {
           const int L = nq[s];
-          if (L == A) maskA |= 1u << s;
           if (L < 0 || L == A) continue;
           bool found = false;
 #pragma unroll
@@ -889,8 +898,7 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
         if (bnd) recA = ldnc64_rec(&a.sp.rec[kb + A]);
 #pragma unroll
         for (int k2 = 0; k2 < 4; k2++)
-          rn[k2] = (need_rn && k2 < nb) ? ldnc64_v4(&a.sp.rec[kb + cb[k2]])
-                                        : make_int4(0, 0, 0, 0);
+          rn[k2] = (need_rn && k2 < nb) ? ldnc64_v4(&a.sp.rec[kb + cb[k2]]) : make_int4(0, 0, 0, 0);
         bool keep = bnd;
         if (bnd && a.gating == 1) keep = ((recA.cq2f >> 16) & F_ACTIVE) != 0u;
         if (!keep) {
@@ -907,12 +915,10 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
           }
           emit = cand && topo_ok;
           if (emit) {
-            int bw = 1, bh = 1;  // E_b edge weights: N/S edges have length bw, W/E bh
             if (PIXEL) {
               d[0] = 1; d[1] = rgb & 0xffu; d[2] = (rgb >> 8) & 0xffu; d[3] = rgb >> 16; d[4] = gx; d[5] = gy;
             } else {
-              bw = bx1 - bx0;
-              bh = by1 - by0;
+              const uint64_t pk = st.bsum32 ? widen_bsum32(pk32) : pk64;
               d[0] = bw * bh;
               d[1] = (int)(pk & 0x1FFFFFull);
               d[2] = (int)((pk >> 21) & 0x1FFFFFull);
@@ -920,7 +926,7 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
               d[4] = bh * ((bw * (2 * bx0 + bw - 1)) / 2);
               d[5] = bw * ((bh * (2 * by0 + bh - 1)) / 2);
             }
-            // weight of the slots in mask s: N (1), S (4) edges have length bw; E (2), W (8) bh
+            // E_b weight of the slots in a mask: N (1), S (4) edges have length bw; E (2), W (8) bh
             auto wsum = [&](unsigned msk) -> int {
               return PIXEL ? __popc(msk) : bw * __popc(msk & 5u) + bh * __popc(msk & 10u);
             };
@@ -965,17 +971,11 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
           }
         }
       }
-      {
-        const unsigned bc = __ballot_sync(FULL, cand), be = __ballot_sync(FULL, emit);
-        const unsigned bs = __ballot_sync(FULL, srej), bp = __ballot_sync(FULL, prop);
-        if (lane == 0) {
-          atomicAdd(&s_cnt[0], __popc(bc));
-          atomicAdd(&s_cnt[1], __popc(be));
-          if (bs) atomicAdd(&s_cnt[3], __popc(bs));
-          if (bp) atomicAdd(&s_cnt[2], __popc(bp));
-        }
-      }
+      r_cand += __popc(__ballot_sync(FULL, cand));  // warp-uniform running counts
+      r_topo += __popc(__ballot_sync(FULL, emit));
+      r_srej += __popc(__ballot_sync(FULL, srej));
       const unsigned pm = __ballot_sync(FULL, prop);
+      r_prop += __popc(pm);
       if (pm) {
         const size_t idx = ((size_t)img * nby + gy) * nbx + gx;
         if (!GATED) {  // size_mode NONE: no budget to check, commit in place
@@ -991,7 +991,7 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
             agg_sums(prop, kb + A, dl, true, a.sp.sums, a.sp.dirty, a.stamp);
             agg_sums(prop, kb + Bm, dl, false, a.sp.sums, a.sp.dirty, a.stamp);
           }
-          if (lane == 0) atomicAdd(&s_cnt[4], __popc(pm));
+          r_commit += __popc(pm);
         } else {
           // HARD / MERGE: A's outflow is subtracted from its budget rem[A]; K5 applies A's moves
           // iff rem[A] >= 0 afterwards (all-or-nothing, A19)
@@ -1016,6 +1016,13 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
   if (GATED) {
     if (lane < pleft) a.props[pbase + lane] = make_uint4(0u, 0xffffffffu, 0u, 0u);
     if (lane + 32 < pleft) a.props[pbase + lane + 32] = make_uint4(0u, 0xffffffffu, 0u, 0u);
+  }
+  if (lane == 0) {
+    if (r_cand) atomicAdd(&s_cnt[0], r_cand);
+    if (r_topo) atomicAdd(&s_cnt[1], r_topo);
+    if (r_prop) atomicAdd(&s_cnt[2], r_prop);
+    if (r_srej) atomicAdd(&s_cnt[3], r_srej);
+    if (r_commit) atomicAdd(&s_cnt[4], r_commit);
   }
   __syncthreads();
   if (threadIdx.x < 5 && s_cnt[threadIdx.x]) atomicAdd(&a.cnt[threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
@@ -1062,7 +1069,7 @@ __global__ void __launch_bounds__(256, 8) k_commit(const PhaseArgs a) {  // 8 CT
       } else {
         rej = true;
         for (int f = 0; f < 6; f++) d[f] = 0;
-        a.sp.dirty[kb + A] = a.stamp;  // so that the next K3 restores rem[A] (and re-derives A's record)
+        mark_dirty(a.sp.dirty, kb + A);  // so that the next K3 restores rem[A] (and re-derives A's record)
         if (a.size_mode == 2) {
           a.sp.victim[kb + A] = 1;
           *a.victim_any = 1u;

@@ -55,4 +55,12 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_co
   -o $OUT/${TAG}_commit -f python tools/profile_one.py --config 4 --n 1 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_snapshot -s 111 -c 1 \
   -o $OUT/${TAG}_snapshot -f python tools/profile_one.py --config 4 --n 1 > /dev/null 2>&1
+# 5. a block stage (b = 2: stage 4, sweep 0, phase 1 -> launch 81 of K4 and K5) and the launch
+#    list without cache flushes (warm L2 as in the graph replay; per-kernel durations)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep -s 81 -c 1 \
+  -o $OUT/${TAG}_sweep_b2 -f python tools/profile_one.py --config 4 --n 1 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_commit -s 81 -c 1 \
+  -o $OUT/${TAG}_commit_b2 -f python tools/profile_one.py --config 4 --n 1 > /dev/null 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -c 4000 --csv \
+  python tools/profile_one.py --config 4 --n 1 > $OUT/${TAG}_launches_nocache.csv 2>/dev/null
 ls -la $OUT/${TAG}_*

@@ -11,7 +11,10 @@
  *
  * Parity pins (tests/test_oracle_*.py): geometry closed forms, brute-force block
  * sums, exhaustive rounding, per-pixel brute-force energy deltas (exact integer
- * equality), exhaustive topology LUT vs flood fill, hand-worked H1, invariants.
+ * equality), exhaustive topology LUT vs flood fill, hand-worked H1-H4, invariants,
+ * and the choices themselves: every Eq. 3 decision and every Eq. 4 merge of random
+ * runs re-derived by brute force (tests/test_oracle_choice.py; one-token mutants of
+ * either argmin fail it, tools/mutation_check.sh).
  * Parity with the paper's own outputs is unpinned (the paper prints none).
  */
 #ifndef RAPID_ORACLE_H

@@ -1,6 +1,7 @@
 """Measure every BASELINE.json config on one GPU: GPU Mpx/s per segmentation (bench.py), the
 sweep roofline fraction, and the single-threaded oracle's Mpx/s on the same input (configs
-1-3 and 5 in full; config 4 on its 8192^2 density-matched sample).  Prints a markdown table.
+1-3 and 5 in full here; config 4's whole-run oracle time from profiles/oracle_full_cfg4.json).
+Prints a markdown table.
 
     python tools/all_configs.py > profiles/<round>_all_configs.md
 """
@@ -21,16 +22,20 @@ for cfg in (1, 2, 3, 4, 5):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", str(cfg), "--steps", "10",
                           "--warmup", "3", "--no-e2e", "--no-cpu"], capture_output=True, text=True, check=True)
     d = json.loads(out.stdout.strip().splitlines()[-1])
-    if cfg == 4:
-        w = synth.scaled(4, 8192, 8192)
-        what = "8192² sample"
-    else:
-        w = synth.config(cfg)
-        what = "full"
+    if cfg == 4:  # the whole config-4 oracle run (106 s, 25 GB) is measured once per round
+        with open(os.path.join(ROOT, "profiles", "oracle_full_cfg4.json")) as f:
+            full = json.load(f)
+        rows.append((cfg, d, full["value"], "full, tools/oracle_full.py", full["seconds"]))
+        continue
+    w = synth.config(cfg)
+    what = "full"
     img = w.images()
+    old = os.sched_getaffinity(0)
+    os.sched_setaffinity(0, {min(old)})  # one core, as taskset -c
     t0 = time.perf_counter()
     oracle.segment(img, w.params)
     dt = time.perf_counter() - t0
+    os.sched_setaffinity(0, old)
     rows.append((cfg, d, w.pixels / dt / 1e6, what, dt))
 
 print("| config | workload | GPU ms / segmentation | GPU Mpx/s | k_sweep frac (pixel stage) | "

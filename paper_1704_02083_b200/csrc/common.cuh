@@ -123,6 +123,21 @@ __device__ __forceinline__ bool simple_point(unsigned m) {
   return c == 1u;
 }
 
+// position of the r-th set bit (0-based) of w; r < popc(w)
+__device__ __forceinline__ unsigned nth_set_bit(uint32_t w, unsigned r) {
+  unsigned pos = 0;
+#pragma unroll
+  for (int h = 16; h > 0; h >>= 1) {
+    const unsigned lo = __popc(w & ((1u << h) - 1u));
+    if (r >= lo) {
+      r -= lo;
+      pos += h;
+      w >>= h;
+    }
+  }
+  return pos;
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -373,11 +373,66 @@ __global__ void __launch_bounds__(256) k_merge_adjacency(const MergeArgs a) {
       if (!((m4 >> k) & 1u) || gx >= nbx) continue;
       const size_t p = (size_t)gy * nbx + gx;
       const int la = map[p];
+      if (!a.sp.victim[kb + la]) continue;  // victims are rare: their neighbours only are loaded
       const int nq[4] = {gy > 0 ? map[p - nbx] : la, gx + 1 < nbx ? map[p + 1] : la,
                          gy + 1 < nby ? map[p + nbx] : la, gx > 0 ? map[p - 1] : la};
       if (nq[0] == la && nq[1] == la && nq[2] == la && nq[3] == la) continue;
-      if (!a.sp.victim[kb + la]) continue;
       const unsigned ew = (unsigned)(st.xs[gx + 1] - st.xs[gx]);
+#pragma unroll
+      for (int d = 0; d < 4; d++)
+        if (nq[d] != la) hash_add(a, kb + la, kb + nq[d], (d & 1) ? eh : ew);
+    }
+  }
+}
+
+// Victim adjacency from the boundary sets, one warp per worklist tile: the tile's 32 bitset words
+// (4 colours x 8 plane rows) hold every gated boundary block at the stage end, a superset of the
+// victims' boundary blocks (a victim passed the static gate); their set bits are dealt 32 at a
+// time to the lanes, each lane loads its block's label and victim flag and, for a victim block
+// only, its four neighbours, adding the shared edge lengths to the (victim, neighbour) hash.
+// Two dependent loads per set bit instead of a full pass over the stage map.
+__global__ void __launch_bounds__(256) k_merge_adj_bset(const MergeArgs a) {
+  if (*a.victim_any == 0u) return;
+  const StageDev &st = a.st;
+  const int nbx = st.nbx, nby = st.nby;
+  const unsigned ntiles = a.worklist ? *a.nwork : (unsigned)(st.tiles_x * st.tiles_y) * (unsigned)a.B;
+  const int lane = lane_id();
+  const unsigned nw = (gridDim.x * blockDim.x) >> 5;
+  for (unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < ntiles; w += nw) {
+    const uint32_t tile = a.worklist ? (uint32_t)a.worklist[w] : w;
+    const uint32_t rr = fdiv(tile, st.fd_tx), img = fdiv(rr, st.fd_ty);
+    const int gx0 = (int)(tile - rr * (uint32_t)st.tiles_x) * TX, gy0 = (int)(rr - img * (uint32_t)st.tiles_y) * TY;
+    const uint32_t word = a.bset[(size_t)tile * 32 + lane];  // colour lane >> 3, plane row lane & 7
+    const unsigned cw = __popc(word);
+    unsigned incl = cw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const unsigned total = __shfl_sync(FULL, incl, 31);
+    const int32_t *map = st.map + (size_t)img * nby * nbx;
+    const int kb = (int)img * a.M;
+    for (unsigned rb = 0; rb < total; rb += 32) {
+      const unsigned k = rb + lane;
+      int j = 0;  // the lane whose word holds set bit k: #lanes with incl <= k
+#pragma unroll
+      for (int h = 16; h > 0; h >>= 1) {
+        const unsigned v = __shfl_sync(FULL, incl, j + h - 1);
+        if (v <= k) j += h;
+      }
+      const uint32_t wj = __shfl_sync(FULL, word, j);
+      const unsigned ej = __shfl_sync(FULL, incl, j) - __popc(wj);
+      if (k >= total) continue;
+      const unsigned bit = nth_set_bit(wj, k - ej);
+      const int gx = gx0 + 2 * (int)bit + ((j >> 3) & 1), gy = gy0 + 2 * (j & 7) + (j >> 4);
+      if (gx >= nbx || gy >= nby) continue;
+      const size_t p = (size_t)gy * nbx + gx;
+      const int la = map[p];
+      if (!a.sp.victim[kb + la]) continue;  // victims are rare: their neighbours only are loaded
+      const int nq[4] = {gy > 0 ? map[p - nbx] : la, gx + 1 < nbx ? map[p + 1] : la,
+                         gy + 1 < nby ? map[p + nbx] : la, gx > 0 ? map[p - 1] : la};
+      const unsigned ew = (unsigned)(st.xs[gx + 1] - st.xs[gx]), eh = (unsigned)(st.ys[gy + 1] - st.ys[gy]);
 #pragma unroll
       for (int d = 0; d < 4; d++)
         if (nq[d] != la) hash_add(a, kb + la, kb + nq[d], (d & 1) ? eh : ew);
@@ -1328,6 +1383,8 @@ void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s) {
   launch_pdl(k_snapshot, dim3(g), dim3(256), s, a);
 }
 
+int g_adj_tma = 0;  // RAPID_ADJ=tma: the victim adjacency from the TMA tile stream instead of the boundary sets
+
 cudaError_t launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int grid, cudaStream_t s,
                         int *nlaunch) {
   const int nchunks = (a.K + CHUNK - 1) / CHUNK;
@@ -1337,7 +1394,8 @@ cudaError_t launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, 
   k_merge_heads<<<grid, 256, 0, s>>>(a);
   const size_t nb = (size_t)a.st.nbx * a.st.nby * a.B;
   (void)nb;
-  if (!launch_merge_adjacency_tma(a, tmap, tgrid, s)) k_merge_adjacency<<<148 * 8, 256, 0, s>>>(a);
+  if (a.bset && g_adj_tma == 0) k_merge_adj_bset<<<148 * 8, 256, 0, s>>>(a);
+  else if (!launch_merge_adjacency_tma(a, tmap, tgrid, s)) k_merge_adjacency<<<148 * 8, 256, 0, s>>>(a);
   k_merge_degree<<<grid, 256, 0, s>>>(a);
   k_merge_scan_deg<<<1, 1024, 0, s>>>(a);
   k_merge_fill<<<grid, 256, 0, s>>>(a);

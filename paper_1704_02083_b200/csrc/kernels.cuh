@@ -327,6 +327,7 @@ void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s);
 // Launch with the programmatic-stream-serialization attribute when g_pdl is set (the kernel must
 // begin with pdl_wait_and_trigger()); a plain stream-ordered launch otherwise.
 extern bool g_pdl;
+extern int g_adj_tma;
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
   cudaLaunchAttribute at[1];

@@ -451,20 +451,6 @@ __device__ __forceinline__ void bset_insert(uint32_t *bset, const StageDev &st, 
   if (ins & 8u) bset_set(bset, st, img, gx - 1, gy);
 }
 
-// position of the r-th set bit (0-based) of w; r < popc(w)
-__device__ __forceinline__ unsigned nth_set_bit(uint32_t w, unsigned r) {
-  unsigned pos = 0;
-#pragma unroll
-  for (int h = 16; h > 0; h >>= 1) {
-    const unsigned lo = __popc(w & ((1u << h) - 1u));
-    if (r >= lo) {
-      r -= lo;
-      pos += h;
-      w >>= h;
-    }
-  }
-  return pos;
-}
 
 // K4 build (once per stage, after the transition): one CTA per sweep tile, thread (r, q) owns
 // the 4 blocks gx0+4q .. gx0+4q+3 of row gy0+r; writes all 32 words of the tile.

@@ -1156,10 +1156,82 @@ __global__ void __launch_bounds__(256) k_bset_dyadic(const TransArgs a) {
   }
 }
 
+// The same boundary sets with one warp per child tile: the warp walks the tile's 8 parent rows
+// top to bottom keeping the resolved rows above and below in registers, so every parent row of
+// the tile (plus one halo row above and below) is loaded, remap-resolved and flag-checked once
+// instead of by three warps; the next row's loads are issued before the current row's words are
+// formed.
+__global__ void __launch_bounds__(256) k_bset_dyadic_rows(const TransArgs a) {
+  const StageDev &pv = a.prev, &nx = a.next;
+  const unsigned ntiles = a.gate ? *a.nwork : (unsigned)(nx.tiles_x * nx.tiles_y) * (unsigned)a.B;
+  const bool rm = *a.remap_pending != 0u;
+  const int lane = lane_id();
+  const unsigned nw = (gridDim.x * blockDim.x) >> 5;
+  for (unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < ntiles; w += nw) {
+    const uint32_t t = a.gate ? (uint32_t)a.worklist[w] : w;
+    const uint32_t rr = fdiv(t, nx.fd_tx), img = fdiv(rr, nx.fd_ty);
+    const int px = (int)(t - rr * (uint32_t)nx.tiles_x) * (TX / 2) + lane;
+    const int tpy = (int)(rr - img * (uint32_t)nx.tiles_y) * (TY / 2);
+    const int kb = (int)img * a.M;
+    const int32_t *pm = pv.map + (size_t)img * pv.nby * pv.nbx;
+    const bool inx = px < pv.nbx;
+    auto res = [&](int p) {
+      return (p >= 0 && rm && !ld64_u8(a.sp.alive + kb + p)) ? (int)ld64_u32(a.sp.remap + kb + p) : p;
+    };
+    // raw labels of parent row py: this lane's column and (lanes 0 / 31) the W / E halo
+    auto load_row = [&](int py, int &L, int &Wh, int &Eh) {
+      const bool iny = py >= 0 && py < pv.nby;
+      const int32_t *row = pm + (size_t)py * pv.nbx;
+      L = (inx && iny) ? row[px] : -1;
+      Wh = (lane == 0 && iny && inx && px > 0) ? row[px - 1] : -1;
+      Eh = (lane == 31 && iny && inx && px + 1 < pv.nbx) ? row[px + 1] : -1;
+    };
+    int Lp, Lc, Wc, Ec, t0, t1;
+    load_row(tpy - 1, Lp, t0, t1);
+    load_row(tpy, Lc, Wc, Ec);
+    Lp = res(Lp);
+    Lc = res(Lc);
+    Wc = res(Wc);
+    Ec = res(Ec);
+    uint32_t *tw = a.bset + (size_t)t * 32;
+#pragma unroll 1
+    for (int r = 0; r < TY / 2; r++) {
+      int Ln, Wn, En;
+      load_row(tpy + r + 1, Ln, Wn, En);  // the next row's loads go out first
+      bool gate = Lc >= 0;
+      if (gate && a.gating == 1) gate = ld64_u8(a.sp.active + kb + Lc) != 0;
+      int Wl = __shfl_up_sync(FULL, Lc, 1), El = __shfl_down_sync(FULL, Lc, 1);
+      if (lane == 0) Wl = Wc;
+      if (lane == 31) El = Ec;
+      const bool dW = Wl >= 0 && Wl != Lc, dE = El >= 0 && El != Lc;
+      const bool dN = Lp >= 0 && Lp != Lc;
+      Ln = res(Ln);
+      const bool dS = Ln >= 0 && Ln != Lc;
+      const unsigned w0 = __ballot_sync(FULL, gate && (dW || dN));  // (cx, cy) = (0, 0)
+      const unsigned w1 = __ballot_sync(FULL, gate && (dE || dN));  // (1, 0)
+      const unsigned w2 = __ballot_sync(FULL, gate && (dW || dS));  // (0, 1)
+      const unsigned w3 = __ballot_sync(FULL, gate && (dE || dS));  // (1, 1)
+      if (lane == 0) {
+        tw[0 * (TY / 2) + r] = w0;
+        tw[1 * (TY / 2) + r] = w1;
+        tw[2 * (TY / 2) + r] = w2;
+        tw[3 * (TY / 2) + r] = w3;
+      }
+      Lp = Lc;
+      Lc = Ln;
+      Wc = res(Wn);
+      Ec = res(En);
+    }
+  }
+}
+
 bool launch_bset_dyadic(const TransArgs &a, int sms, cudaStream_t s) {
   if (!(a.prev.uniform && a.next.uniform && a.prev.b == 2 * a.next.b && a.bset)) return false;
   const unsigned ntiles = (unsigned)(a.next.tiles_x * a.next.tiles_y) * (unsigned)a.B;
-  k_bset_dyadic<<<std::min<unsigned>(ntiles, (unsigned)sms * 8), 256, 0, s>>>(a);
+  if (g_bset_rows && ntiles >= 32768u)  // (small stages: too few tiles for a warp each; measured)
+    k_bset_dyadic_rows<<<std::min<unsigned>((ntiles + 7) / 8, (unsigned)sms * 8), 256, 0, s>>>(a);
+  else
+    k_bset_dyadic<<<std::min<unsigned>(ntiles, (unsigned)sms * 8), 256, 0, s>>>(a);
   return true;
 }
 
@@ -1383,6 +1455,7 @@ void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s) {
   launch_pdl(k_snapshot, dim3(g), dim3(256), s, a);
 }
 
+int g_bset_rows = 1;  // RAPID_BSET_ROWS=0: the warp-per-parent-row boundary-set pass (k_bset_dyadic)
 int g_adj_tma = 0;  // RAPID_ADJ=tma: the victim adjacency from the TMA tile stream instead of the boundary sets
 
 cudaError_t launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int grid, cudaStream_t s,

@@ -32,7 +32,7 @@ def make_ctx(env, pixels, sps):
 
 VARIANTS = [{}, {"RAPID_NO_GRAPH": "1"}, {"RAPID_SWEEP": "scan"}, {"RAPID_FUSE_BSET": "1"}, {"RAPID_FUSE_SNAP": "1"},
             {"RAPID_NO_TMA": "1"}, {"RAPID_BSET_PARENT": "0"}, {"RAPID_SWEEP_NO_SMALLB": "1"},
-            {"RAPID_PDL": "1"}, {"RAPID_ADJ": "tma"}]
+            {"RAPID_PDL": "1"}, {"RAPID_ADJ": "tma"}, {"RAPID_BSET_ROWS": "0"}]
 
 
 @pytest.mark.parametrize("cfg,side", [(2, 1024), (4, 1024), (5, 0)])

@@ -94,7 +94,7 @@ struct rapid_ctx {
   uint32_t *mlock = nullptr, *res = nullptr;
   Ctl *ctl = nullptr;
   // plan-sized buffers
-  DevBuf tab, bsum, maps[2], props, work, cands, bset;
+  DevBuf tab, bsum, maps[2], props, work, cands, bset, vtile;
   // host-API staging
   DevBuf himg, hlab;
   // occupancy
@@ -397,6 +397,7 @@ int build_plan(rapid_ctx *c, int H, int W, const rapid_params *p) {
   if ((rc = ensure(c, c->cands, cand_max * 32))) return rc;
   if ((rc = ensure(c, c->work, N.tiles_max * 4))) return rc;
   if ((rc = ensure(c, c->bset, N.tiles_max * 32 * 4))) return rc;  // 1 bit per block
+  if ((rc = ensure(c, c->vtile, N.tiles_max))) return rc;           // victim-tile marks (stage stamps)
   cudaError_t e = cudaMemcpy(c->tab.p, N.tab.data(), N.tab.size() * 4, cudaMemcpyHostToDevice);
   if ((rc = cuda_check(c, e, "upload tables"))) return rc;
   N.valid = true;
@@ -504,6 +505,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
   cudaMemsetAsync(ctl, 0, sizeof(Ctl), s);
   // the dirty bitmap starts empty every call (a captured graph replays)
   cudaMemsetAsync(c->dirty, 0, sizeof(uint32_t) * ((K + 31) / 32 + 1), s);
+  cudaMemsetAsync(c->vtile.p, 0, c->vtile.bytes, s);  // victim-tile marks (stamped per stage)
 
   StageDev sd[MAXS];
   struct alignas(64) TMap {
@@ -749,6 +751,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       ma.npairs = &ctl->npairs;
       ma.flag = ctl->mflag;
       ma.bset = c->use_bset ? (const uint32_t *)c->bset.p : nullptr;
+      ma.vtile = (uint8_t *)c->vtile.p;
+      ma.vstamp = (uint8_t)(st + 1);
       ma.stage_info = &ctl->stage_info[st][0];
       const cudaError_t me = launch_merge_round(ma, has_tmap[st] ? tmaps[st].b : nullptr, c->tiles_grid, grid_k, s, &c->launches);
       if (me != cudaSuccess) return fail(c, RAPID_E_CUDA, std::string("cooperative launch k_merge_match: ") + cudaGetErrorString(me));
@@ -804,6 +808,10 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     const bool last_work = nst > 1 && tile_gate;
     fa.worklist = last_work ? (const int32_t *)c->work.p : nullptr;
     fa.nwork = &ctl->nwork[nst - 1];
+    if (last_work && c->use_bset && g_adj_tma == 0 && p->size_mode == RAPID_SIZE_MERGE) {
+      fa.vtile = (const uint8_t *)c->vtile.p;  // marked by the last stage's adjacency pass
+      fa.vstamp = (uint8_t)nst;
+    }
     launch_final(fa, P.st[nst - 1].b > 1, s);
     c->launches++;
   }
@@ -853,7 +861,7 @@ void rapid_free(rapid_ctx *c) {
                   c->vlist, c->alist, c->pairs, c->alive, c->active, c->victim, c->y, c->dirty,
                   c->deg, c->chunk, c->hkeys, c->candE, c->hvals, c->hnext, c->candT, c->ctl,
                   c->candV, c->mlock, c->res,
-                  c->tab.p, c->bsum.p, c->maps[0].p, c->maps[1].p, c->props.p, c->work.p, c->cands.p, c->bset.p,
+                  c->tab.p, c->bsum.p, c->maps[0].p, c->maps[1].p, c->props.p, c->work.p, c->cands.p, c->bset.p, c->vtile.p,
                   c->himg.p, c->hlab.p};
   for (void *q : ptrs)
     if (q) cudaFree(q);

@@ -430,6 +430,7 @@ __global__ void __launch_bounds__(256) k_merge_adj_bset(const MergeArgs a) {
       const size_t p = (size_t)gy * nbx + gx;
       const int la = map[p];
       if (!a.sp.victim[kb + la]) continue;  // victims are rare: their neighbours only are loaded
+      if (a.vtile) a.vtile[tile] = a.vstamp;  // (the final remap visits marked tiles only)
       const int nq[4] = {gy > 0 ? map[p - nbx] : la, gx + 1 < nbx ? map[p + 1] : la,
                          gy + 1 < nby ? map[p + nbx] : la, gx > 0 ? map[p - 1] : la};
       const unsigned ew = (unsigned)(st.xs[gx + 1] - st.xs[gx]), eh = (unsigned)(st.ys[gy + 1] - st.ys[gy]);
@@ -1287,54 +1288,81 @@ __global__ void k_final_upsample(const FinalArgs a) {
 
 __global__ void __launch_bounds__(128) k_final_remap(const FinalArgs a) {
   // in place on the map of `last` (== labels); merged-away labels only occur in worklist
-  // tiles at gated stages (victims are active superpixels).  Persistent CTAs, one tile per
-  // iteration; a thread reads 4 consecutive labels of 2 rows (16-B loads when rows allow),
+  // tiles at gated stages (victims are active superpixels).  Persistent CTAs; chunks of 128
+  // worklist tiles: with the adjacency pass's marks (vtile) every thread first decides one tile —
+  // no merged-away superpixel has a boundary block there, so either none has a block there at
+  // all or one covers the whole tile (a tile holding blocks of two labels has a boundary block
+  // of each): its first block decides — and the CTA then rewrites the tiles that need it, one
+  // per iteration: a thread reads 4 consecutive labels of 2 rows (16-B loads when rows allow)
   // and writes back only labels whose superpixel was merged away.
   if (*a.remap_pending == 0u) return;
+  __shared__ uint32_t s_need[128];
+  __shared__ unsigned s_n;
   const StageDev &st = a.last;
   const unsigned ntiles = a.worklist ? *a.nwork : (unsigned)(st.tiles_x * st.tiles_y) * (unsigned)a.B;
   const bool vec = (st.nbx & 3) == 0;
   const int u = threadIdx.x;
-  for (unsigned w = blockIdx.x; w < ntiles; w += gridDim.x) {
-    const uint32_t tile = a.worklist ? (uint32_t)a.worklist[w] : w;
-    const uint32_t r = fdiv(tile, st.fd_tx), img = fdiv(r, st.fd_ty);
-    const int gx = (int)(tile - r * (uint32_t)st.tiles_x) * TX + 4 * (u & 15);
-    const int gy0 = (int)(r - img * (uint32_t)st.tiles_y) * TY + 2 * (u >> 4);
-    const int kb = (int)img * a.M;
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const int gy = gy0 + h;
-      if (gy >= st.nby || gx >= st.nbx) continue;
-      int32_t *p = a.labels + ((size_t)img * st.nby + gy) * st.nbx + gx;
-      int l[4];
-      if (vec) {
-        const int4 v = *reinterpret_cast<const int4 *>(p);
-        l[0] = v.x; l[1] = v.y; l[2] = v.z; l[3] = v.w;
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; k++) l[k] = gx + k < st.nbx ? p[k] : -1;
-      }
-      bool dirty = false;
-      int last = -1, res = -1;
-#pragma unroll
-      for (int k = 0; k < 4; k++) {
-        if (l[k] < 0) continue;
-        if (l[k] != last) {
-          last = l[k];
-          res = a.sp.alive[kb + last] ? last : a.sp.remap[kb + last];
+  for (unsigned c0 = blockIdx.x * 128u; c0 < ntiles; c0 += gridDim.x * 128u) {
+    if (u == 0) s_n = 0;
+    __syncthreads();
+    {
+      const unsigned w = c0 + u;
+      if (w < ntiles) {
+        const uint32_t tile = a.worklist ? (uint32_t)a.worklist[w] : w;
+        bool need = true;
+        if (a.vtile && a.vtile[tile] != a.vstamp) {
+          const uint32_t r = fdiv(tile, st.fd_tx), img = fdiv(r, st.fd_ty);
+          const int tx0 = (int)(tile - r * (uint32_t)st.tiles_x) * TX, ty0 = (int)(r - img * (uint32_t)st.tiles_y) * TY;
+          const int l0 = a.labels[((size_t)img * st.nby + ty0) * st.nbx + tx0];
+          need = !a.sp.alive[(int)img * a.M + l0];
         }
-        dirty |= res != l[k];
-        l[k] = res;
-      }
-      if (!dirty) continue;
-      if (vec) {
-        *reinterpret_cast<int4 *>(p) = make_int4(l[0], l[1], l[2], l[3]);
-      } else {
-#pragma unroll
-        for (int k = 0; k < 4; k++)
-          if (gx + k < st.nbx) p[k] = l[k];
+        if (need) s_need[atomicAdd(&s_n, 1u)] = tile;
       }
     }
+    __syncthreads();
+    const unsigned nneed = s_n;
+    for (unsigned k = 0; k < nneed; k++) {
+      const uint32_t tile = s_need[k];
+      const uint32_t r = fdiv(tile, st.fd_tx), img = fdiv(r, st.fd_ty);
+      const int gx = (int)(tile - r * (uint32_t)st.tiles_x) * TX + 4 * (u & 15);
+      const int gy0 = (int)(r - img * (uint32_t)st.tiles_y) * TY + 2 * (u >> 4);
+      const int kb = (int)img * a.M;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int gy = gy0 + h;
+        if (gy >= st.nby || gx >= st.nbx) continue;
+        int32_t *p = a.labels + ((size_t)img * st.nby + gy) * st.nbx + gx;
+        int l[4];
+        if (vec) {
+          const int4 v = *reinterpret_cast<const int4 *>(p);
+          l[0] = v.x; l[1] = v.y; l[2] = v.z; l[3] = v.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; q++) l[q] = gx + q < st.nbx ? p[q] : -1;
+        }
+        bool dirty = false;
+        int last = -1, res = -1;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          if (l[q] < 0) continue;
+          if (l[q] != last) {
+            last = l[q];
+            res = a.sp.alive[kb + last] ? last : a.sp.remap[kb + last];
+          }
+          dirty |= res != l[q];
+          l[q] = res;
+        }
+        if (!dirty) continue;
+        if (vec) {
+          *reinterpret_cast<int4 *>(p) = make_int4(l[0], l[1], l[2], l[3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; q++)
+            if (gx + q < st.nbx) p[q] = l[q];
+        }
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -1467,7 +1495,9 @@ cudaError_t launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, 
   k_merge_heads<<<grid, 256, 0, s>>>(a);
   const size_t nb = (size_t)a.st.nbx * a.st.nby * a.B;
   (void)nb;
-  if (a.bset && g_adj_tma == 0) k_merge_adj_bset<<<148 * 8, 256, 0, s>>>(a);
+  if (a.bset && g_adj_tma == 0) {
+    k_merge_adj_bset<<<148 * 8, 256, 0, s>>>(a);
+  }
   else if (!launch_merge_adjacency_tma(a, tmap, tgrid, s)) k_merge_adjacency<<<148 * 8, 256, 0, s>>>(a);
   k_merge_degree<<<grid, 256, 0, s>>>(a);
   k_merge_scan_deg<<<1, 1024, 0, s>>>(a);

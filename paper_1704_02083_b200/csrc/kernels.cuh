@@ -52,6 +52,8 @@ struct MergeArgs {
   unsigned int *chunk;       // per-chunk counts -> offsets
   unsigned int *total;       // number of victims
   int32_t *vlist;            // ordered victims
+  uint8_t *vtile;            // per stage tile: = vstamp if it holds a victim's boundary block (or null)
+  uint8_t vstamp;
   // adjacency hash
   unsigned long long *hkeys;
   unsigned int *hvals;
@@ -176,6 +178,8 @@ struct FinalArgs {
   int32_t *labels;           // [B][H][W]
   const int32_t *worklist;   // remap pass: active tiles of `last` (null: every tile)
   const unsigned int *nwork;
+  const uint8_t *vtile = nullptr;  // tiles marked by the last merge round's adjacency pass (or null)
+  uint8_t vstamp = 0;
 };
 
 // ---- f4 quality metrics (quality.cu)

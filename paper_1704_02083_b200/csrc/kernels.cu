@@ -451,45 +451,49 @@ __global__ void k_merge_degree(const MergeArgs a) {
   }
 }
 
-// exclusive scan of deg[0..nv) by a single CTA (victims per stage are few)
-__global__ void k_merge_scan_deg(const MergeArgs a) {
+// exclusive scan of deg[0..nv) by a single CTA (victims per stage are few): warp w owns the
+// contiguous segment w of 32; pass 1 sums each segment with coalesced loads, the 32 segment
+// sums are scanned, pass 2 rescans each segment from its offset and writes it
+__global__ void __launch_bounds__(1024) k_merge_scan_deg(const MergeArgs a) {
   if (*a.victim_any == 0u) return;
-  __shared__ unsigned warp_tot[32];
-  __shared__ unsigned carry;
+  __shared__ unsigned seg_tot[32];
   const int nv = (int)*a.total;
-  if (threadIdx.x == 0) carry = 0;
+  const int warp = threadIdx.x >> 5, lane = lane_id(), nwarps = blockDim.x >> 5;
+  const int per = ((nv + nwarps - 1) / nwarps + 31) & ~31;
+  const int b0 = min(nv, warp * per), b1 = min(nv, b0 + per);
+  unsigned sum = 0;
+  for (int i = b0 + lane; i < b1; i += 32) sum += a.deg[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+  if (lane == 0) seg_tot[warp] = sum;
   __syncthreads();
-  for (int base = 0; base < nv; base += blockDim.x) {
-    const int i = base + threadIdx.x;
-    unsigned v = i < nv ? a.deg[i] : 0u;
+  if (warp == 0) {
+    unsigned t = lane < nwarps ? seg_tot[lane] : 0u;
+    const unsigned own = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(FULL, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nwarps) seg_tot[lane] = t - own;  // exclusive segment offsets
+    if (lane == 31) {
+      a.deg[nv] = t;
+      *a.deg_total = t;
+    }
+  }
+  __syncthreads();
+  unsigned carry = seg_tot[warp];
+  for (int base = b0; base < b1; base += 32) {
+    const int i = base + lane;
+    const unsigned v = i < b1 ? a.deg[i] : 0u;
     unsigned x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      unsigned y = __shfl_up_sync(FULL, x, o);
-      if (lane_id() >= o) x += y;
+      const unsigned y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
     }
-    if (lane_id() == 31) warp_tot[threadIdx.x >> 5] = x;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      const int nw = blockDim.x >> 5;
-      unsigned t = threadIdx.x < nw ? warp_tot[threadIdx.x] : 0u;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        unsigned y = __shfl_up_sync(FULL, t, o);
-        if (lane_id() >= o) t += y;
-      }
-      warp_tot[threadIdx.x] = t;
-    }
-    __syncthreads();
-    const unsigned woff = (threadIdx.x >> 5) ? warp_tot[(threadIdx.x >> 5) - 1] : 0u;
-    if (i < nv) a.deg[i] = carry + woff + x - v;
-    __syncthreads();
-    if (threadIdx.x == 0) carry += warp_tot[(blockDim.x >> 5) - 1];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    a.deg[nv] = carry;
-    *a.deg_total = carry;
+    if (i < b1) a.deg[i] = carry + x - v;
+    carry += __shfl_sync(FULL, x, 31);
   }
 }
 

@@ -423,14 +423,22 @@ __global__ void __launch_bounds__(256) k_merge_adj_bset(const MergeArgs a) {
       }
       const uint32_t wj = __shfl_sync(FULL, word, j);
       const unsigned ej = __shfl_sync(FULL, incl, j) - __popc(wj);
-      if (k >= total) continue;
-      const unsigned bit = nth_set_bit(wj, k - ej);
-      const int gx = gx0 + 2 * (int)bit + ((j >> 3) & 1), gy = gy0 + 2 * (j & 7) + (j >> 4);
-      if (gx >= nbx || gy >= nby) continue;
+      int gx = 0, gy = 0, la = -1;
+      bool vic = false;
+      if (k < total) {
+        const unsigned bit = nth_set_bit(wj, k - ej);
+        gx = gx0 + 2 * (int)bit + ((j >> 3) & 1);
+        gy = gy0 + 2 * (j & 7) + (j >> 4);
+        if (gx < nbx && gy < nby) {
+          la = map[(size_t)gy * nbx + gx];
+          vic = a.sp.victim[kb + la] != 0;  // victims are rare: their neighbours only are loaded
+        }
+      }
+      const unsigned vm = __ballot_sync(FULL, vic);
+      if (vm == 0u) continue;  // warp-uniform
+      if (a.vtile && lane == __ffs(vm) - 1) a.vtile[tile] = a.vstamp;  // (the final remap visits marked tiles only)
+      if (!vic) continue;
       const size_t p = (size_t)gy * nbx + gx;
-      const int la = map[p];
-      if (!a.sp.victim[kb + la]) continue;  // victims are rare: their neighbours only are loaded
-      if (a.vtile) a.vtile[tile] = a.vstamp;  // (the final remap visits marked tiles only)
       const int nq[4] = {gy > 0 ? map[p - nbx] : la, gx + 1 < nbx ? map[p + 1] : la,
                          gy + 1 < nby ? map[p + nbx] : la, gx > 0 ? map[p - 1] : la};
       const unsigned ew = (unsigned)(st.xs[gx + 1] - st.xs[gx]), eh = (unsigned)(st.ys[gy + 1] - st.ys[gy]);
@@ -1324,16 +1332,19 @@ __global__ void __launch_bounds__(128) k_final_remap(const FinalArgs a) {
       }
     }
     __syncthreads();
+    // the needed tiles, a warp each (4 at a time per CTA): lane l takes 4 consecutive labels of
+    // row (l >> 4) + 2 h of the tile, h = 0..7
     const unsigned nneed = s_n;
-    for (unsigned k = 0; k < nneed; k++) {
+    const int lane = u & 31;
+    for (unsigned k = (unsigned)(u >> 5); k < nneed; k += 4) {
       const uint32_t tile = s_need[k];
       const uint32_t r = fdiv(tile, st.fd_tx), img = fdiv(r, st.fd_ty);
-      const int gx = (int)(tile - r * (uint32_t)st.tiles_x) * TX + 4 * (u & 15);
-      const int gy0 = (int)(r - img * (uint32_t)st.tiles_y) * TY + 2 * (u >> 4);
+      const int gx = (int)(tile - r * (uint32_t)st.tiles_x) * TX + 4 * (lane & 15);
+      const int gy0 = (int)(r - img * (uint32_t)st.tiles_y) * TY + (lane >> 4);
       const int kb = (int)img * a.M;
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int gy = gy0 + h;
+#pragma unroll 2
+      for (int h = 0; h < TY / 2; h++) {
+        const int gy = gy0 + 2 * h;
         if (gy >= st.nby || gx >= st.nbx) continue;
         int32_t *p = a.labels + ((size_t)img * st.nby + gy) * st.nbx + gx;
         int l[4];

@@ -503,8 +503,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
   c->stopped = false;
   c->stop_map = nullptr;
   cudaMemsetAsync(ctl, 0, sizeof(Ctl), s);
-  // the dirty bitmap starts empty every call (a captured graph replays)
-  cudaMemsetAsync(c->dirty, 0, sizeof(uint32_t) * ((K + 31) / 32 + 1), s);
+  // the dirty byte map starts empty every call (a captured graph replays)
+  cudaMemsetAsync(c->dirty, 0, (size_t)K + 4, s);
   cudaMemsetAsync(c->vtile.p, 0, c->vtile.bytes, s);  // victim-tile marks (stamped per stage)
 
   StageDev sd[MAXS];
@@ -637,7 +637,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       Timer tm(c, s, RAPID_K_PHASESET, st);
       {
         Timer t2(c, s, RAPID_K_SNAPSHOT, st);
-        SnapArgs sa{sp, K, 0u, (long long)p->l_num, (long long)p->l_den};
+        SnapArgs sa{sp, K, 0u, (long long)p->l_num, gated_sz ? (long long)p->l_den : 0ll};
         launch_snapshot(sa, grid_k, s);
         c->launches++;
       }
@@ -645,7 +645,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
         for (int ph = 0; ph < 4; ph++, g++) {
           if (!(t == 0 && ph == 0) && !fused_snap) {  // (fused: the previous commit refreshed them)
             Timer t2(c, s, RAPID_K_SNAPSHOT, st);
-            SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, (long long)p->l_den,
+            SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, gated_sz ? (long long)p->l_den : 0ll,
                         t > 0 ? &ctl->cnt[st][t - 1][0][0] : nullptr};
             launch_snapshot(sa, grid_k, s);
             c->launches++;
@@ -698,11 +698,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
               const cudaError_t e = launch_commit_snap(pa, pixel, c->sm_count, s);
               if (e != cudaSuccess) return fail(c, RAPID_E_CUDA, std::string("cooperative launch k_commit<SNAP>: ") + cudaGetErrorString(e));
             } else {
-              // latency-bound gathers: up to full occupancy, but no more CTAs than ~4 proposals
-              // each at most (a phase proposes at most a quarter of the stage's blocks)
-              const long long maxp = ((long long)B * sd[st].nbx * sd[st].nby + 3) / 4;
-              const int cgrid = (int)std::min<long long>(c->sm_count * 8, std::max<long long>(c->sm_count, (maxp + 1023) / 1024));
-              launch_commit(pa, pixel, cgrid, s);
+              launch_commit(pa, pixel, c->sm_count * 8, s);  // latency-bound gathers: full occupancy
             }
             c->launches++;
           }
@@ -713,7 +709,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     {  // snapshot of the last phase's changes (merge round / prediction read it)
       Timer t2(c, s, RAPID_K_SNAPSHOT, st);
       if (g > 0 && !fused_snap) {
-        SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, (long long)p->l_den,
+        SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, gated_sz ? (long long)p->l_den : 0ll,
                     sweeps > 0 ? &ctl->cnt[st][sweeps - 1][0][0] : nullptr};
         launch_snapshot(sa, grid_k, s);
         c->launches++;
@@ -763,7 +759,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     }
     if (st == 0 && mask != RAPID_MASK_OFF) {
       Timer tm(c, s, RAPID_K_PREDICT, st);
-      SnapArgs sa{sp, K, 0u, (long long)p->l_num, (long long)p->l_den};
+      SnapArgs sa{sp, K, 0u, (long long)p->l_num, gated_sz ? (long long)p->l_den : 0ll};
       launch_snapshot(sa, grid_k, s);
       c->launches++;
       PredictArgs pr;

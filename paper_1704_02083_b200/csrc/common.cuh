@@ -86,7 +86,7 @@ struct SpDev {
   int8_t *y;                 // [K]
   uint8_t *victim;           // [K]
   int32_t *out;              // [K] rem: outflow budget left in the current phase (O6', A19)
-  uint32_t *dirty;           // [(K + 31) / 32] bitmap: superpixels whose sums (or budget) changed this phase
+  uint32_t *dirty;           // byte map [K] (as words): superpixels whose sums (or budget) changed this phase
   int32_t *remap;            // [K]
 };
 
@@ -261,7 +261,7 @@ __device__ __forceinline__ void red_add_keep(unsigned long long *p, unsigned lon
 }
 
 __device__ __forceinline__ void mark_dirty(uint32_t *dirty, int key) {
-  atomicOr(&dirty[key >> 5], 1u << (key & 31));
+  reinterpret_cast<uint8_t *>(dirty)[key] = 1u;  // byte map: a plain store, no atomic
 }
 
 __device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[6], bool negate,

@@ -233,7 +233,6 @@ __global__ void k_stats0(const InitArgs a) {
 // ------------------------------------------------------------------ K3: snapshot
 __global__ void __launch_bounds__(256, 8) k_snapshot(const SnapArgs a) {  // one wave at K = 2^20
   pdl_wait_and_trigger();
-  if (sweep_skipped(a.prev)) return;
   snapshot_warps(a, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, (gridDim.x * blockDim.x) >> 5);
 }
 
@@ -1314,10 +1313,13 @@ __global__ void __launch_bounds__(128) k_final_remap(const FinalArgs a) {
   const unsigned ntiles = a.worklist ? *a.nwork : (unsigned)(st.tiles_x * st.tiles_y) * (unsigned)a.B;
   const bool vec = (st.nbx & 3) == 0;
   const int u = threadIdx.x;
-  for (unsigned c0 = blockIdx.x * 128u; c0 < ntiles; c0 += gridDim.x * 128u) {
+  // tiles decided per CTA iteration: up to 128 with marks (about ntiles / grid, so that every CTA
+  // has work), one without (every tile is needed)
+  const unsigned chunk = a.vtile ? max(1u, min(128u, ntiles / gridDim.x)) : 1u;
+  for (unsigned c0 = blockIdx.x * chunk; c0 < ntiles; c0 += gridDim.x * chunk) {
     if (u == 0) s_n = 0;
     __syncthreads();
-    {
+    if ((unsigned)u < chunk) {
       const unsigned w = c0 + u;
       if (w < ntiles) {
         const uint32_t tile = a.worklist ? (uint32_t)a.worklist[w] : w;
@@ -1335,16 +1337,19 @@ __global__ void __launch_bounds__(128) k_final_remap(const FinalArgs a) {
     // the needed tiles, a warp each (4 at a time per CTA): lane l takes 4 consecutive labels of
     // row (l >> 4) + 2 h of the tile, h = 0..7
     const unsigned nneed = s_n;
-    const int lane = u & 31;
-    for (unsigned k = (unsigned)(u >> 5); k < nneed; k += 4) {
+    // a single needed tile: all 4 warps on it (rows 2 g + (lane >> 4) + 8 h); several: a warp each
+    const bool one = nneed == 1u;
+    const int lane = u & 31, g = u >> 5;
+    for (unsigned k = one ? 0u : (unsigned)g; k < nneed; k += one ? 1u : 4u) {
       const uint32_t tile = s_need[k];
       const uint32_t r = fdiv(tile, st.fd_tx), img = fdiv(r, st.fd_ty);
       const int gx = (int)(tile - r * (uint32_t)st.tiles_x) * TX + 4 * (lane & 15);
-      const int gy0 = (int)(r - img * (uint32_t)st.tiles_y) * TY + (lane >> 4);
+      const int gy0 = (int)(r - img * (uint32_t)st.tiles_y) * TY + (lane >> 4) + (one ? 2 * g : 0);
       const int kb = (int)img * a.M;
+      const int nh = one ? 2 : TY / 2, step = one ? 8 : 2;
 #pragma unroll 2
-      for (int h = 0; h < TY / 2; h++) {
-        const int gy = gy0 + 2 * h;
+      for (int h = 0; h < nh; h++) {
+        const int gy = gy0 + step * h;
         if (gy >= st.nby || gx >= st.nbx) continue;
         int32_t *p = a.labels + ((size_t)img * st.nby + gy) * st.nbx + gx;
         int l[4];
@@ -1510,7 +1515,7 @@ cudaError_t launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, 
   k_merge_heads<<<grid, 256, 0, s>>>(a);
   const size_t nb = (size_t)a.st.nbx * a.st.nby * a.B;
   (void)nb;
-  if (a.bset && g_adj_tma == 0) {
+  if (a.bset && a.worklist && g_adj_tma == 0) {  // (ungated stages: dense sets, the tile stream is faster)
     k_merge_adj_bset<<<148 * 8, 256, 0, s>>>(a);
   }
   else if (!launch_merge_adjacency_tma(a, tmap, tgrid, s)) k_merge_adjacency<<<148 * 8, 256, 0, s>>>(a);

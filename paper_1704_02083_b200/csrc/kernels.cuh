@@ -207,7 +207,11 @@ bool launch_pyramid_leaf24(const StageDev &st, const StageDev &up, const uint8_t
 void launch_init_map0(const InitArgs &a, cudaStream_t s);
 void launch_stats0(const InitArgs &a, cudaStream_t s);
 // ------------------------------------------------------------------ K3: snapshot (device side)
-__device__ __forceinline__ Rec make_rec(const SpDev &sp, int k) {
+#ifndef RAPID_FULLREC
+#define RAPID_FULLREC 0
+#endif
+constexpr bool kFullRec = RAPID_FULLREC;
+__device__ __forceinline__ Rec make_rec(const SpDev &sp, int k, bool full = true) {
   // gathers with a 64-B L2 fill (ld64_*, common.cuh); coherent: the fused commit + snapshot
   // kernel reads sums its own atomics wrote
   const ulonglong2 s01 = ld64_v2u64(sp.sums + (size_t)k * SUMW), s23 = ld64_v2u64(sp.sums + (size_t)k * SUMW + 2);
@@ -216,9 +220,19 @@ __device__ __forceinline__ Rec make_rec(const SpDev &sp, int k) {
   const unsigned long long n = s[0];
   Rec r;
   r.n = (int32_t)n;
-  r.init = (int32_t)ld64_u32(sp.init + k);
-  const uint32_t flags = ld64_u8(sp.alive + k) | (ld64_u8(sp.active + k) << 1) |
-                         ((uint32_t)((int)(int8_t)ld64_u8(sp.y + k) + 1) << 2);
+  uint32_t flags;
+  if (full) {
+    r.init = (int32_t)ld64_u32(sp.init + k);
+    flags = ld64_u8(sp.alive + k) | (ld64_u8(sp.active + k) << 1) |
+            ((uint32_t)((int)(int8_t)ld64_u8(sp.y + k) + 1) << 2);
+  } else {
+    // inside a stage's phase loop InitSize and the alive / active / y flags do not change (merges
+    // and prediction come after the stage's last snapshot, and every stage starts with a full
+    // refresh): one 32-B sector of the previous record instead of four flag-table gathers
+    const int4 o0 = ld64_v4(&sp.rec[k]), o1 = ld64_v4(reinterpret_cast<const int4 *>(&sp.rec[k]) + 1);
+    r.init = o1.y;
+    flags = (uint32_t)o0.w >> 16;
+  }
   uint32_t c0 = 0, c1 = 0, c2 = 0;
   int32_t mx = 0, my = 0;
   if (n > 0) {
@@ -260,18 +274,19 @@ __device__ __forceinline__ Rec make_rec(const SpDev &sp, int k) {
 // (n_snap - o) l_den >= l_num InitSize, i.e. o <= rem = floor((n_snap l_den - l_num InitSize) / l_den);
 // K4 subtracts each proposal from rem[A], so K5 accepts A's proposals iff rem[A] >= 0 after K4
 __device__ __forceinline__ int32_t outflow_budget(const Rec &r, long long l_num, long long l_den) {
-  if (l_den <= 0) return 0;
+  if (l_den <= 0) return 0;  // (size mode NONE: no budget)
   const long long S = (long long)r.n * l_den - l_num * (long long)r.init;
+  if ((l_den & (l_den - 1)) == 0) return (int32_t)(S >> (63 - __clzll(l_den)));  // floor, power of 2
   long long q = S / l_den;
   if (q * l_den > S) q--;  // floor for negative S
   return (int32_t)q;
 }
 
-// Full refresh (stamp 0) or only the superpixels marked in the dirty bitmap (one bit per
-// superpixel, set by the commits of the previous phase), by warps wid = 0 .. nw-1.  A warp takes
-// 128 consecutive superpixels (4 bitmap words; lane l looks at the 4-bit slice l of them and
-// clears the words it read), compacts the marked ones and refreshes them 32 at a time (one record
-// per lane).  Also run at the end of the commit kernel (after a grid barrier).
+// Full refresh (stamp 0) or only the superpixels marked in the dirty byte map (set by the commits
+// of the previous phase with plain stores), by warps wid = 0 .. nw-1.  A warp takes 128
+// consecutive superpixels (lane l reads the 4 bytes of superpixels 4l .. 4l+3 as one word and
+// clears it), compacts the marked ones and refreshes them 32 at a time (one record per lane).
+// Also run at the end of the commit kernel (after a grid barrier).
 __device__ __forceinline__ void snapshot_warps(const SnapArgs &a, int wid, int nw) {
   const int lane = lane_id();
   const int n4 = (a.K + 3) >> 2;
@@ -280,16 +295,17 @@ __device__ __forceinline__ void snapshot_warps(const SnapArgs &a, int wid, int n
     const int i = ch * 32 + lane;  // 4-superpixel slice: superpixels 4i .. 4i+3
     unsigned m = 0;
     if (i < n4) {
-      uint32_t *wp = a.sp.dirty + (i >> 3);
+      uint32_t *wp = a.sp.dirty + i;
       const uint32_t wv = *wp;
       if (a.stamp == 0u) {
 #pragma unroll
         for (int j = 0; j < 4; j++)
           if (4 * i + j < a.K) m |= 1u << j;
       } else {
-        m = (wv >> (4 * (i & 7))) & 0xfu;
+        m = (unsigned)((wv & 0xffu) != 0u) | ((unsigned)((wv & 0xff00u) != 0u) << 1) |
+            ((unsigned)((wv & 0xff0000u) != 0u) << 2) | ((unsigned)((wv & 0xff000000u) != 0u) << 3);
       }
-      if ((lane & 7) == 0 && wv != 0u) *wp = 0u;  // every bit of the word is handled in this chunk
+      if (wv != 0u) *wp = 0u;
     }
     unsigned incl = __popc(m);
 #pragma unroll
@@ -317,7 +333,7 @@ __device__ __forceinline__ void snapshot_warps(const SnapArgs &a, int wid, int n
         }
         bit = __ffs(mm) - 1;
         const int k = 4 * (ch * 32 + j) + bit;
-        const Rec r = make_rec(a.sp, k);
+        const Rec r = make_rec(a.sp, k, a.stamp == 0u || kFullRec);
         // the outflow budget of the next phase starts full: every superpixel whose rem[] the
         // last phase lowered (every proposal's source) was marked dirty by K4 or K5
         a.sp.out[k] = outflow_budget(r, a.l_num, a.l_den);

@@ -637,7 +637,12 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       Timer tm(c, s, RAPID_K_PHASESET, st);
       {
         Timer t2(c, s, RAPID_K_SNAPSHOT, st);
-        SnapArgs sa{sp, K, 0u, (long long)p->l_num, gated_sz ? (long long)p->l_den : 0ll};
+        // full refresh at stage 0, after prediction (every flag changed) and whenever the stats
+        // are re-derived (RECOUNT / PYRAMID); otherwise only the previous merge round changed
+        // records since the last snapshot, and it marked its victims and targets dirty
+        const bool full = st == 0 || (st == 1 && mask != RAPID_MASK_OFF) || p->stats_mode != RAPID_STATS_REUSE;
+        SnapArgs sa{sp, K, full ? 0u : 1u, (long long)p->l_num, gated_sz ? (long long)p->l_den : 0ll};
+        sa.full_flags = true;
         launch_snapshot(sa, grid_k, s);
         c->launches++;
       }

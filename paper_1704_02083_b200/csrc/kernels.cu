@@ -635,6 +635,8 @@ __global__ void k_merge_apply(const MergeArgs a) {
     a.sp.active[A] = 0;
     a.sp.y[A] = 0;
     a.sp.remap[A] = T % a.M;  // local id of the target
+    mark_dirty(a.sp.dirty, A);  // (the next stage's first snapshot refreshes only these)
+    mark_dirty(a.sp.dirty, T);
     a.mlock[A] = 0u;
     a.mlock[T] = 0u;
   }

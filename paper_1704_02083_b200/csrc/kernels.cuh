@@ -36,8 +36,9 @@ struct SnapArgs {
   int32_t K;
   uint32_t stamp;             // 0: refresh all; else only the superpixels marked in the dirty bitmap
   long long l_num, l_den;     // size floor l (the outflow budget rem[] of the next phase)
-  const unsigned long long *prev = nullptr;  // counters of the previous sweep: a skipped sweep (A25)
-                                             // changed nothing, so there is nothing to refresh
+  const unsigned long long *prev = nullptr;  // (unused)
+  bool full_flags = false;    // dirty refresh that reads InitSize and flags from their tables
+                              // (stage start after a merge round) instead of the old record
 };
 
 struct MergeArgs {
@@ -333,7 +334,7 @@ __device__ __forceinline__ void snapshot_warps(const SnapArgs &a, int wid, int n
         }
         bit = __ffs(mm) - 1;
         const int k = 4 * (ch * 32 + j) + bit;
-        const Rec r = make_rec(a.sp, k, a.stamp == 0u || kFullRec);
+        const Rec r = make_rec(a.sp, k, a.stamp == 0u || a.full_flags || kFullRec);
         // the outflow budget of the next phase starts full: every superpixel whose rem[] the
         // last phase lowered (every proposal's source) was marked dirty by K4 or K5
         a.sp.out[k] = outflow_budget(r, a.l_num, a.l_den);

@@ -934,10 +934,7 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
             if (hv && bestE < 0) {
               if (GATED && ((long long)recA.n - d[0]) * a.l_den < a.l_num * (long long)recA.init) {
                 srej = true;  // A12: the desired move would leave A below l * InitSize
-                if (a.size_mode == 2) {
-                  a.sp.victim[kb + A] = 1;
-                  *a.victim_any = 1u;
-                }
+                if (a.size_mode == 2) a.sp.victim[kb + A] = 1;  // (victim_any: once per warp below)
               } else {
                 prop = true;
                 Bm = bestB;
@@ -959,7 +956,13 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
       }
       r_cand += __popc(__ballot_sync(FULL, cand));  // warp-uniform running counts
       r_topo += __popc(__ballot_sync(FULL, emit));
-      r_srej += __popc(__ballot_sync(FULL, srej));
+      {
+        const unsigned bs = __ballot_sync(FULL, srej);
+        r_srej += __popc(bs);
+        // one store per warp round to the stage's victim flag (a store by every rejecting lane
+        // serialises on the one address)
+        if (bs && a.size_mode == 2 && lane == 0) *a.victim_any = 1u;
+      }
       const unsigned pm = __ballot_sync(FULL, prop);
       r_prop += __popc(pm);
       if (pm) {
@@ -1056,12 +1059,10 @@ __global__ void __launch_bounds__(256, 8) k_commit(const PhaseArgs a) {  // 8 CT
         rej = true;
         for (int f = 0; f < 6; f++) d[f] = 0;
         mark_dirty(a.sp.dirty, kb + A);  // so that the next K3 restores rem[A] (and re-derives A's record)
-        if (a.size_mode == 2) {
-          a.sp.victim[kb + A] = 1;
-          *a.victim_any = 1u;
-        }
+        if (a.size_mode == 2) a.sp.victim[kb + A] = 1;
       }
     }
+    if (a.size_mode == 2 && __ballot_sync(FULL, rej) && lane_id() == 0) *a.victim_any = 1u;  // once per warp
     if (PIXEL || a.st.b <= 4) {  // warp-uniform
       agg_sums_small(ok, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp);
       agg_sums_small(ok, kb + B, d, false, a.sp.sums, a.sp.dirty, a.stamp);

@@ -50,24 +50,27 @@ def main(rep, kregex, func, top=40):
     rows = list(csv.reader(raw.splitlines()))
     hdr = next(r for r in rows if "Address" in r)
     ia, ii, iw = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
+    it = hdr.index("Thread Instructions Executed")
     body = [r for r in rows[rows.index(hdr) + 1:] if len(r) > iw and r[ia].startswith("0x")]
     base = int(body[0][ia], 16)
-    inst, stall = collections.Counter(), collections.Counter()
+    inst, stall, thr = collections.Counter(), collections.Counter(), collections.Counter()
     for r in body:
         off = int(r[ia], 16) - base
         key = lm.get(off, ("?", 0))
         inst[key] += float(r[ii] or 0)
         stall[key] += float(r[iw] or 0)
+        thr[key] += float(r[it] or 0)
     ti, ts = sum(inst.values()), sum(stall.values())
     src = {}
-    print(f"{'file:line':24s} {'inst%':>6s} {'stall%':>6s}")
+    print(f"{'file:line':24s} {'inst%':>6s} {'stall%':>6s} {'thr/inst':>8s}")
     for key in sorted(inst, key=lambda k: -(inst[k] / ti + stall[k] / ts))[:int(top)]:
         f, ln = key
         if f not in src and f != "?":
             p = os.path.join(ROOT, "paper_1704_02083_b200", "csrc", f)
             src[f] = open(p).read().splitlines() if os.path.exists(p) else []
         text = src.get(f, [])[ln - 1].strip()[:80] if f in src and 0 < ln <= len(src[f]) else ""
-        print(f"{f + ':' + str(ln):24s} {100 * inst[key] / ti:6.1f} {100 * stall[key] / ts:6.1f}  {text}")
+        simd = thr[key] / inst[key] if inst[key] else 0.0
+        print(f"{f + ':' + str(ln):24s} {100 * inst[key] / ti:6.1f} {100 * stall[key] / ts:6.1f} {simd:8.1f}  {text}")
     print(f"total warp instructions {ti:.0f}, stall samples {ts:.0f}")
 
 

@@ -650,8 +650,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
         for (int ph = 0; ph < 4; ph++, g++) {
           if (!(t == 0 && ph == 0) && !fused_snap) {  // (fused: the previous commit refreshed them)
             Timer t2(c, s, RAPID_K_SNAPSHOT, st);
-            SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, gated_sz ? (long long)p->l_den : 0ll,
-                        t > 0 ? &ctl->cnt[st][t - 1][0][0] : nullptr};
+            SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, gated_sz ? (long long)p->l_den : 0ll};
             launch_snapshot(sa, grid_k, s);
             c->launches++;
           }
@@ -714,8 +713,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     {  // snapshot of the last phase's changes (merge round / prediction read it)
       Timer t2(c, s, RAPID_K_SNAPSHOT, st);
       if (g > 0 && !fused_snap) {
-        SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, gated_sz ? (long long)p->l_den : 0ll,
-                    sweeps > 0 ? &ctl->cnt[st][sweeps - 1][0][0] : nullptr};
+        SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, gated_sz ? (long long)p->l_den : 0ll};
         launch_snapshot(sa, grid_k, s);
         c->launches++;
       }

@@ -164,8 +164,8 @@ __device__ __forceinline__ void pdl_wait_and_trigger() {
 // __match_any_sync groups the lanes by key, every group is reduced at once with REDUX
 // (__reduce_add_sync on 16-bit halves: each d[f] is in [0, 2^47), so no 32-bit partial sum
 // overflows), and each group's leader issues fire-and-forget int64 atomics.  Integer
-// atomics are order-independent, so the result is deterministic.  The leader also stamps the
-// superpixel dirty (the next snapshot refreshes stamped records only).
+// atomics are order-independent, so the result is deterministic.  The leader also marks the
+// superpixel dirty (the next snapshot refreshes marked records only).
 // Must be called by all 32 lanes (uniform control flow).
 // Runs of adjacent lanes with equal keys (invalid lanes get unique keys): run start of this
 // lane and whether it ends its run.  Full-mask intrinsics only (a per-group mask makes the
@@ -265,7 +265,7 @@ __device__ __forceinline__ void mark_dirty(uint32_t *dirty, int key) {
 }
 
 __device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[6], bool negate,
-                                         unsigned long long *sums, uint32_t *dirty, uint32_t stamp) {
+                                         unsigned long long *sums, uint32_t *dirty) {
   if (__ballot_sync(FULL, valid) == 0u) return;  // warp-uniform
   const WarpRun run = warp_runs(valid, key);
   const int lane = lane_id();
@@ -297,7 +297,7 @@ __device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[
 // <= 16 x 32), colour sums (18 bits each; <= 255 x 16 x 32), position sums (26 bits each;
 // <= 2^20 x 32) — so the segmented scan moves 2 words instead of 6.
 __device__ __forceinline__ void agg_sums_small(bool valid, int key, const long long d[6], bool negate,
-                                               unsigned long long *sums, uint32_t *dirty, uint32_t stamp) {
+                                               unsigned long long *sums, uint32_t *dirty) {
   if (__ballot_sync(FULL, valid) == 0u) return;  // warp-uniform
   const int lane = lane_id();
   unsigned long long u0 = 0, u1 = 0;

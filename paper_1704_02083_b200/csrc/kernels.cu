@@ -226,7 +226,7 @@ __global__ void k_stats0(const InitArgs a) {
       else block_data_blk(st, img, gx, gy, d);
       key = img * a.M + st.map[t];
     }
-    agg_sums(valid, key, d, false, a.sp.sums, nullptr, 0);
+    agg_sums(valid, key, d, false, a.sp.sums, nullptr);
   }
 }
 
@@ -1269,7 +1269,7 @@ __global__ void k_recount(const RecountArgs a) {
       else block_data_blk(st, img, gx, gy, d);
       key = img * a.M + st.map[t];
     }
-    agg_sums(valid, key, d, false, a.rc, nullptr, 0);
+    agg_sums(valid, key, d, false, a.rc, nullptr);
   }
 }
 
@@ -1500,7 +1500,7 @@ void launch_stats0(const InitArgs &a, cudaStream_t s) {
 }
 
 void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s) {
-  // one pass: every warp checks 128 stamps once (grid capped at `grid` x 2)
+  // one pass: every warp checks 128 superpixels' dirty bytes once (grid capped at `grid` x 2)
   const int g = grid_for(((size_t)a.K + 127) / 128 * 32, 256, 2 * grid);
   launch_pdl(k_snapshot, dim3(g), dim3(256), s, a);
 }

@@ -34,9 +34,8 @@ struct PhaseArgs {
 struct SnapArgs {
   SpDev sp;
   int32_t K;
-  uint32_t stamp;             // 0: refresh all; else only the superpixels marked in the dirty bitmap
+  uint32_t stamp;             // 0: refresh all; else only the superpixels marked in the dirty byte map
   long long l_num, l_den;     // size floor l (the outflow budget rem[] of the next phase)
-  const unsigned long long *prev = nullptr;  // (unused)
   bool full_flags = false;    // dirty refresh that reads InitSize and flags from their tables
                               // (stage start after a merge round) instead of the old record
 };

@@ -395,8 +395,8 @@ __global__ void __launch_bounds__(K4B_THREADS, K4B_MIN_BLOCKS) k_eval(const Phas
       const size_t idx = ((size_t)img * nby + gy) * nbx + gx;
       if (!GATED) {  // size_mode NONE: no budget to check, commit in place
         if (prop) a.st.map[idx] = Bm;
-        agg_sums(prop, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp);
-        agg_sums(prop, kb + Bm, d, false, a.sp.sums, a.sp.dirty, a.stamp);
+        agg_sums(prop, kb + A, d, true, a.sp.sums, a.sp.dirty);
+        agg_sums(prop, kb + Bm, d, false, a.sp.sums, a.sp.dirty);
         c_commit += __popc(pm);
       } else {  // outflow budget, as in k_sweep
         agg_add_i32(prop, kb + A, -(int)d[0], a.sp.out);
@@ -974,11 +974,11 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
           }
           const long long dl[6] = {d[0], d[1], d[2], d[3], d[4], d[5]};
           if (PIXEL || st.b <= 4) {  // warp-uniform
-            agg_sums_small(prop, kb + A, dl, true, a.sp.sums, a.sp.dirty, a.stamp);
-            agg_sums_small(prop, kb + Bm, dl, false, a.sp.sums, a.sp.dirty, a.stamp);
+            agg_sums_small(prop, kb + A, dl, true, a.sp.sums, a.sp.dirty);
+            agg_sums_small(prop, kb + Bm, dl, false, a.sp.sums, a.sp.dirty);
           } else {
-            agg_sums(prop, kb + A, dl, true, a.sp.sums, a.sp.dirty, a.stamp);
-            agg_sums(prop, kb + Bm, dl, false, a.sp.sums, a.sp.dirty, a.stamp);
+            agg_sums(prop, kb + A, dl, true, a.sp.sums, a.sp.dirty);
+            agg_sums(prop, kb + Bm, dl, false, a.sp.sums, a.sp.dirty);
           }
           r_commit += __popc(pm);
         } else {
@@ -1021,14 +1021,14 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
 // O6' (A19): the proposals of source A commit iff A's total outflow fits its budget, i.e. iff
 // rem[A] >= 0 after K4 subtracted every proposal of A (all-or-nothing; one 4-B gather from the
 // small budget table per proposal).  Accepted moves are applied here: label, boundary-set bits,
-// warp-aggregated sums; a rejected source is stamped dirty (its budget is restored next phase).
+// warp-aggregated sums; a rejected source is marked dirty (its budget is restored next phase).
 // SNAP (cooperative launch, every CTA resident): after a grid barrier the same CTAs refresh the
-// records stamped dirty in this phase (K3 of the next phase / of the stage end, without a launch)
+// records marked dirty in this phase (K3 of the next phase / of the stage end, without a launch)
 template <bool PIXEL, bool SNAP>
 __global__ void __launch_bounds__(256, 8) k_commit(const PhaseArgs a) {  // 8 CTAs/SM: the grid is one wave
   pdl_wait_and_trigger();
   const unsigned long long n = cta_count(a.prev, a.prop_count, !SNAP);
-  if (n == 0) return;  // SNAP: grid-uniform (an empty list stamps nothing to refresh)
+  if (n == 0) return;  // SNAP: grid-uniform (an empty list marks nothing to refresh)
   unsigned c_commit = 0, c_rej = 0;
   for (unsigned long long base = blockIdx.x * 256ull; base < n; base += gridDim.x * 256ull) {
     const unsigned long long i = base + threadIdx.x;
@@ -1064,11 +1064,11 @@ __global__ void __launch_bounds__(256, 8) k_commit(const PhaseArgs a) {  // 8 CT
     }
     if (a.size_mode == 2 && __ballot_sync(FULL, rej) && lane_id() == 0) *a.victim_any = 1u;  // once per warp
     if (PIXEL || a.st.b <= 4) {  // warp-uniform
-      agg_sums_small(ok, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp);
-      agg_sums_small(ok, kb + B, d, false, a.sp.sums, a.sp.dirty, a.stamp);
+      agg_sums_small(ok, kb + A, d, true, a.sp.sums, a.sp.dirty);
+      agg_sums_small(ok, kb + B, d, false, a.sp.sums, a.sp.dirty);
     } else {
-      agg_sums(ok, kb + A, d, true, a.sp.sums, a.sp.dirty, a.stamp);
-      agg_sums(ok, kb + B, d, false, a.sp.sums, a.sp.dirty, a.stamp);
+      agg_sums(ok, kb + A, d, true, a.sp.sums, a.sp.dirty);
+      agg_sums(ok, kb + B, d, false, a.sp.sums, a.sp.dirty);
     }
     c_commit += __popc(__ballot_sync(FULL, ok));
     c_rej += __popc(__ballot_sync(FULL, rej));

@@ -281,3 +281,13 @@ def test_config4_strip_reaches_64bit_block_stage(rapid):
     o, lab, sp, info = assert_parity(rapid, w.images(), w.params)
     s16 = w.params.block_sizes.index(16)
     assert o.counters[s16, ..., oracle.C_COMMIT].sum() > 100  # the 64-bit stage really moves blocks
+
+
+def test_maximum_sweeps_and_stages(rapid):
+    """The largest sweep count the ABI accepts (64, most of them skipped by the exact early exit)
+    and a 7-stage list up to the largest block size, under MERGE with a mask: bit-exact, and the
+    per-phase counters of every executed sweep equal the oracle's."""
+    img = synth.image(144, 208, 77, 9, 60, 300)
+    p = P(24, [64, 32, 16, 8, 4, 2, 1], 64, size_mode=2, mask=1, tau2=3000)
+    o, lab, sp, info = assert_parity(rapid, img, p)
+    assert max(int(x) for x in info.stage_sweeps_run[:7]) < 64  # the early exit did stop stages

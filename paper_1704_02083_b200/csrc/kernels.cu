@@ -1242,7 +1242,8 @@ __global__ void __launch_bounds__(256) k_bset_dyadic_rows(const TransArgs a) {
 bool launch_bset_dyadic(const TransArgs &a, int sms, cudaStream_t s) {
   if (!(a.prev.uniform && a.next.uniform && a.prev.b == 2 * a.next.b && a.bset)) return false;
   const unsigned ntiles = (unsigned)(a.next.tiles_x * a.next.tiles_y) * (unsigned)a.B;
-  if (g_bset_rows && ntiles >= 32768u)  // (small stages: too few tiles for a warp each; measured)
+  // (small stages: too few tiles for a warp each, measured; RAPID_BSET_ROWS=2 forces it for tests)
+  if ((g_bset_rows && ntiles >= 32768u) || g_bset_rows == 2)
     k_bset_dyadic_rows<<<std::min<unsigned>((ntiles + 7) / 8, (unsigned)sms * 8), 256, 0, s>>>(a);
   else
     k_bset_dyadic<<<std::min<unsigned>(ntiles, (unsigned)sms * 8), 256, 0, s>>>(a);
@@ -1505,7 +1506,7 @@ void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s) {
   launch_pdl(k_snapshot, dim3(g), dim3(256), s, a);
 }
 
-int g_bset_rows = 1;  // RAPID_BSET_ROWS=0: the warp-per-parent-row boundary-set pass (k_bset_dyadic)
+int g_bset_rows = 1;  // RAPID_BSET_ROWS=0: the warp-per-parent-row boundary-set pass (k_bset_dyadic); 2: rows everywhere
 int g_adj_tma = 0;  // RAPID_ADJ=tma: the victim adjacency from the TMA tile stream instead of the boundary sets
 
 cudaError_t launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int grid, cudaStream_t s,

@@ -32,7 +32,8 @@ def make_ctx(env, pixels, sps):
 
 VARIANTS = [{}, {"RAPID_NO_GRAPH": "1"}, {"RAPID_SWEEP": "scan"}, {"RAPID_FUSE_BSET": "1"}, {"RAPID_FUSE_SNAP": "1"},
             {"RAPID_NO_TMA": "1"}, {"RAPID_BSET_PARENT": "0"}, {"RAPID_SWEEP_NO_SMALLB": "1"},
-            {"RAPID_PDL": "1"}, {"RAPID_ADJ": "tma"}, {"RAPID_BSET_ROWS": "0"}]
+            {"RAPID_PDL": "1"}, {"RAPID_ADJ": "tma"}, {"RAPID_BSET_ROWS": "0"},
+            {"RAPID_BSET_ROWS": "2"}]
 
 
 @pytest.mark.parametrize("cfg,side", [(2, 1024), (4, 1024), (5, 0)])
@@ -244,3 +245,15 @@ def test_host_stream_long_run_drains_flag_ring():
         r.close()
     for k in range(n):
         assert np.array_equal(labs[k], oracle.segment(imgs[k], p).labels), f"image {k}"
+
+
+def test_random_cases_through_row_walking_bset_pass():
+    """The row-walking parent-map boundary-set pass runs only on stages with >= 32768 tiles by
+    default (configs 3 and 4); forced everywhere (RAPID_BSET_ROWS=2) the randomized all-options
+    sweep — ragged tiles, batches, every mask rule — stays bit-exact with the oracle."""
+    from test_gpu_parity import random_all_options
+    r = make_ctx({"RAPID_BSET_ROWS": "2"}, 1 << 22, 1 << 16)
+    try:
+        random_all_options(r, 79, 24)
+    finally:
+        r.close()

@@ -229,6 +229,20 @@ class Clocks:
         except Exception:
             self.p = None
 
+    def wait_ready(self, timeout=10.0):
+        """Block until nvidia-smi has written its first sample (its start-up can take longer than
+        a short timed region), so that the samples cover the timed region."""
+        if self.p is None:
+            return
+        t0 = time.time()
+        while time.time() - t0 < timeout:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    return
+            except OSError:
+                pass
+            time.sleep(0.02)
+
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -308,6 +322,8 @@ def run_ours(args):
     r.set_profiling(0)
     r.segment(img, p, labels)  # capture + instantiate the graph outside the timed region
     clocks = Clocks(local) if rank == 0 else None
+    if clocks:
+        clocks.wait_ready()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()

@@ -475,7 +475,7 @@ def run_ours(args):
                 "setting": args.setting,
                 "quality": quality,
                 "alive": int(info.alive), "active": int(info.active)}
-        if not args.no_cpu:
+        if not args.no_cpu and world == 1:  # (the oracle runs on rank 0 at N = 1 only)
             line["cpu_baseline"] = cpu_baseline(args.config, args.sample, args.setting)
         print(json.dumps(line), flush=True)
     r.close()

@@ -291,3 +291,15 @@ def test_maximum_sweeps_and_stages(rapid):
     p = P(24, [64, 32, 16, 8, 4, 2, 1], 64, size_mode=2, mask=1, tau2=3000)
     o, lab, sp, info = assert_parity(rapid, img, p)
     assert max(int(x) for x in info.stage_sweeps_run[:7]) < 64  # the early exit did stop stages
+
+
+@pytest.mark.parametrize("mask,stats,size_mode", [(2, 0, 2), (3, 0, 2), (1, 1, 2), (1, 2, 2), (1, 0, 1), (0, 1, 1)])
+def test_config4_density_options_at_2048(rapid, mask, stats, size_mode):
+    """Config 4's densities at 2048^2 (4096 superpixels, 2048 worklist-sized tiles at the pixel
+    stage) under the other mask rules (BSP, EQ7), stats modes (RECOUNT, PYRAMID) and size modes
+    (HARD with and without the mask): bit-exact with the oracle, counters included."""
+    w = synth.scaled(4, 2048, 2048)
+    p = copy.deepcopy(w.params)
+    p.mask_rule, p.stats_mode, p.size_mode = mask, stats, size_mode
+    o, lab, sp, info = assert_parity(rapid, w.images(), p)
+    assert info.status == 0

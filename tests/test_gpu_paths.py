@@ -257,3 +257,25 @@ def test_random_cases_through_row_walking_bset_pass():
         random_all_options(r, 79, 24)
     finally:
         r.close()
+
+
+def test_host_stream_batches():
+    """rapid_segment_host_stream with batches (B = 3 images per segmentation call, 4 calls):
+    every image of every call equals the oracle's."""
+    import torch
+    w = synth.scaled(5, 256, 256, B=3)
+    imgs, labs, refs = [], [], []
+    for k in range(4):
+        wk = synth.scaled(5, 256, 256, B=3, seed_offset=10 * k)
+        h = torch.empty((3, 256, 256, 3), dtype=torch.uint8).pin_memory()
+        wk.images(out=h.numpy())
+        imgs.append(h.numpy())
+        labs.append(torch.empty((3, 256, 256), dtype=torch.int32).pin_memory().numpy())
+        refs.append(oracle.segment(imgs[-1], w.params).labels)
+    r = make_ctx({}, w.pixels, w.B * w.params.n_superpixels)
+    try:
+        r.segment_host_stream(imgs, w.params, labs)
+    finally:
+        r.close()
+    for k in range(4):
+        assert np.array_equal(labs[k], refs[k]), f"call {k}"

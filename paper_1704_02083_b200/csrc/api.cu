@@ -28,6 +28,7 @@ struct Ctl {  // per-segmentation device control block (zeroed at the start of e
   unsigned int vtotal, deg_total, npairs, atotal;
   unsigned int mflag[2];  // cooperative merge match: pending flags per round parity
   unsigned int wq[MAXS * MAXSW * 4];  // k_sweep work-queue counters, one per phase
+  unsigned int big;  // K3: some snapshot size exceeded the call's packed-delta limit (K5 then REDs the sums)
 };
 
 struct StagePlan {
@@ -36,6 +37,7 @@ struct StagePlan {
   size_t o_xs = 0, o_ys = 0, o_px = 0, o_py = 0, o_cxs = 0, o_cys = 0;
   size_t bsum_off = 0;  // in uint64 elements
   bool smallb = false;  // block stage with (max block area) x (max coordinate) < 2^22: K4's 32-bit position factors
+  int32_t maxn_lim = 0;  // uniform stages: K5 packs its deltas while every snapshot size is <= this
 };
 
 struct Plan {
@@ -78,7 +80,7 @@ struct rapid_ctx {
   uint32_t stamp_base = 1;
   int launches = 0;
   // per-superpixel arrays (cap_sp)
-  unsigned long long *sums = nullptr, *rc = nullptr;
+  unsigned long long *sums = nullptr, *rc = nullptr, *dsum = nullptr;
   Rec *rec = nullptr;
   int32_t *init = nullptr, *out = nullptr, *remap = nullptr;
   int32_t *head = nullptr, *vlist = nullptr, *alist = nullptr, *pairs = nullptr;
@@ -101,6 +103,9 @@ struct rapid_ctx {
   int scan_grid = 0, eval_grid = 0, sweep_grid = 0, tiles_grid = 0;  // persistent grid sizes (CTAs)
   int sweep_tail = 25;  // RAPID_SWEEP_TAIL: % of K4's words dealt in quarter-size groups at the end (block stages)
   int sweep_gpw = 2;  // K4 word groups per warp (RAPID_SWEEP_GPW overrides, A/B testing)
+  int snap_ctas = 4;  // RAPID_SNAP_CTAS: K3 CTAs per SM
+  bool packed = true;  // RAPID_PACKED=0: K5 always issues the six int64 REDs per run on the sums
+  int packed_lim = 0;  // RAPID_PACKED_LIM=n (> 0): caps the stages' size limits (tests the per-phase switch)
   bool fuse_snap = false;  // RAPID_FUSE_SNAP=1: K3 of the next phase runs at the end of a cooperative K5 (measured: same step time)
   bool bset_parent = true;  // dyadic stages: boundary sets from the parent map (RAPID_BSET_PARENT=0: child-map tile pass)
   bool no_smallb = false;   // RAPID_SWEEP_NO_SMALLB=1: every block stage takes K4's 64-bit position-factor variant (parity-tested variant)
@@ -332,6 +337,16 @@ int build_plan(rapid_ctx *c, int H, int W, const rapid_params *p) {
     for (int i = 0; i < S.nbx; i++) mw = std::max<int64_t>(mw, S.xs[i + 1] - S.xs[i]);
     for (int j = 0; j < S.nby; j++) mh = std::max<int64_t>(mh, S.ys[j + 1] - S.ys[j]);
     S.smallb = !c->no_smallb && S.b > 1 && mw * mh * (int64_t)(std::max(H, W) - 1) < (int64_t(1) << 22);
+    // K5's packed deltas: in one phase a superpixel S loses at most n_S pixels and gains at most
+    // 4 n_S R (every incoming block is a 4-neighbour of one of S's blocks, which do not move in
+    // the phase; R = largest / smallest block area), so each field of its phase total stays below
+    // 4 R n_S max(255, W - 1, H - 1) in magnitude: int32 while n_S <= maxn_lim
+    int64_t nw = INT64_MAX, nh = INT64_MAX;
+    for (int i = 0; i < S.nbx; i++) nw = std::min<int64_t>(nw, S.xs[i + 1] - S.xs[i]);
+    for (int j = 0; j < S.nby; j++) nh = std::min<int64_t>(nh, S.ys[j + 1] - S.ys[j]);
+    const int64_t R = (mw * mh + nw * nh - 1) / (nw * nh);
+    const int64_t vmax = std::max<int64_t>(255, std::max(H, W) - 1);
+    S.maxn_lim = (int32_t)std::min<int64_t>(INT32_MAX, (int64_t)INT32_MAX / (4 * R * vmax));
   }
   for (int s = 0; s < nst; s++) {
     StagePlan &S = N.st[s];
@@ -447,6 +462,9 @@ SpDev sp_dev(rapid_ctx *c) {
   d.out = c->out;
   d.dirty = c->dirty;
   d.remap = c->remap;
+  d.dsum = c->dsum;
+  d.big = &c->ctl->big;
+  d.nlim = 0;  // set per call from the plan (enqueue)
   return d;
 }
 
@@ -496,6 +514,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
   const int gated_sz = p->size_mode != RAPID_SIZE_NONE;
   const bool fused_snap = gated_sz && c->fuse_snap;  // K3 folded into the previous K5
   const int grid_k = c->sm_count * 4;
+  const int grid_snap = c->sm_count * c->snap_ctas;  // K3 (RAPID_SNAP_CTAS per SM)
   Ctl *ctl = c->ctl;
   c->launches = 0;
   c->evs.clear();
@@ -505,6 +524,9 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
   cudaMemsetAsync(ctl, 0, sizeof(Ctl), s);
   // the dirty byte map starts empty every call (a captured graph replays)
   cudaMemsetAsync(c->dirty, 0, (size_t)K + 4, s);
+  // K5's packed deltas start (and end every phase) folded: cleared per call so that a call
+  // stopped at a debug point cannot leak into the next
+  if (c->packed) cudaMemsetAsync(c->dsum, 0, (size_t)K * 32, s);
   cudaMemsetAsync(c->vtile.p, 0, c->vtile.bytes, s);  // victim-tile marks (stamped per stage)
 
   StageDev sd[MAXS];
@@ -517,7 +539,14 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     sd[st] = stage_dev(c, st, labels);
     has_tmap[st] = c->use_tma && make_label_tmap(tmaps[st].b, sd[st].map, sd[st].nbx, sd[st].nby, B);
   }
-  const SpDev sp = sp_dev(c);
+  SpDev sp = sp_dev(c);
+  {  // K5's packed deltas: the call's size limit is the smallest stage limit (0 / null: off)
+    int lim = INT32_MAX;
+    for (int st = 0; st < (int)P.nst; st++) lim = std::min(lim, (int)P.st[st].maxn_lim);
+    if (c->packed_lim > 0) lim = std::min(lim, c->packed_lim);
+    sp.nlim = lim;
+    if (!c->packed || lim <= 0) sp.dsum = nullptr;
+  }
   const int32_t *T = (const int32_t *)c->tab.p;
 
   InitArgs ia;
@@ -643,7 +672,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
         const bool full = st == 0 || (st == 1 && mask != RAPID_MASK_OFF) || p->stats_mode != RAPID_STATS_REUSE;
         SnapArgs sa{sp, K, full ? 0u : 1u, (long long)p->l_num, gated_sz ? (long long)p->l_den : 0ll};
         sa.full_flags = true;
-        launch_snapshot(sa, grid_k, s);
+        launch_snapshot(sa, grid_snap, s);
         c->launches++;
       }
       for (int t = 0; t < sweeps; t++) {
@@ -651,7 +680,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           if (!(t == 0 && ph == 0) && !fused_snap) {  // (fused: the previous commit refreshed them)
             Timer t2(c, s, RAPID_K_SNAPSHOT, st);
             SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, gated_sz ? (long long)p->l_den : 0ll};
-            launch_snapshot(sa, grid_k, s);
+            launch_snapshot(sa, grid_snap, s);
             c->launches++;
           }
           PhaseArgs pa;
@@ -706,7 +735,13 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
             }
             c->launches++;
           }
-          if (stop_at(RAPID_STOP_PHASE, st, t, ph)) return RAPID_OK;
+          if (stop_at(RAPID_STOP_PHASE, st, t, ph)) {
+            if (gated_sz && !fused_snap) {  // fold K5's packed deltas: the stats read at the stop are whole
+              SnapArgs sa{sp, K, c->stamp_base + (uint32_t)g, (long long)p->l_num, (long long)p->l_den};
+              launch_snapshot(sa, grid_snap, s);
+            }
+            return RAPID_OK;
+          }
         }
       }
     }
@@ -714,7 +749,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       Timer t2(c, s, RAPID_K_SNAPSHOT, st);
       if (g > 0 && !fused_snap) {
         SnapArgs sa{sp, K, c->stamp_base + (uint32_t)(g - 1), (long long)p->l_num, gated_sz ? (long long)p->l_den : 0ll};
-        launch_snapshot(sa, grid_k, s);
+        launch_snapshot(sa, grid_snap, s);
         c->launches++;
       }
     }
@@ -763,7 +798,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     if (st == 0 && mask != RAPID_MASK_OFF) {
       Timer tm(c, s, RAPID_K_PREDICT, st);
       SnapArgs sa{sp, K, 0u, (long long)p->l_num, gated_sz ? (long long)p->l_den : 0ll};
-      launch_snapshot(sa, grid_k, s);
+      launch_snapshot(sa, grid_snap, s);
       c->launches++;
       PredictArgs pr;
       pr.st = sd[st];
@@ -856,7 +891,7 @@ void rapid_free(rapid_ctx *c) {
   if (c->herr) cudaFreeHost(c->herr);
   for (DevBuf *b : {&c->himg2, &c->hlab2, &c->qkeys, &c->qcnt, &c->qsize, &c->qspb, &c->qacc})
     if (b->p) cudaFree(b->p);
-  void *ptrs[] = {c->sums, c->rc, c->rec, c->init, c->out, c->remap, c->head,
+  void *ptrs[] = {c->sums, c->rc, c->dsum, c->rec, c->init, c->out, c->remap, c->head,
                   c->vlist, c->alist, c->pairs, c->alive, c->active, c->victim, c->y, c->dirty,
                   c->deg, c->chunk, c->hkeys, c->candE, c->hvals, c->hnext, c->candT, c->ctl,
                   c->candV, c->mlock, c->res,
@@ -899,7 +934,7 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
       (rc = dalloc(c, &c->hvals, hc)) || (rc = dalloc(c, &c->hnext, hc)) ||
       (rc = dalloc(c, &c->candT, hc)) || (rc = dalloc(c, &c->candE, 2 * hc)) ||
       (rc = dalloc(c, &c->candV, hc)) || (rc = dalloc(c, &c->mlock, K)) || (rc = dalloc(c, &c->res, K)) ||
-      (rc = dalloc(c, &c->ctl, 1))) {
+      (rc = dalloc(c, &c->ctl, 1)) || (rc = dalloc(c, &c->dsum, K * 4))) {
     rapid_free(c);
     return rc;
   }
@@ -913,6 +948,9 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   c->eval_grid = c->sm_count * eval_occupancy();
   c->sweep_grid = c->sm_count * sweep_occupancy();
   if (const char *e = getenv("RAPID_SWEEP_GPW")) c->sweep_gpw = std::max(1, atoi(e));
+  if (const char *e = getenv("RAPID_PACKED")) c->packed = e[0] != '0';
+  if (const char *e = getenv("RAPID_SNAP_CTAS")) c->snap_ctas = std::min(8, std::max(1, atoi(e)));
+  if (const char *e = getenv("RAPID_PACKED_LIM")) c->packed_lim = std::max(0, atoi(e));
   if (const char *e = getenv("RAPID_SWEEP_TAIL")) c->sweep_tail = std::min(100, std::max(0, atoi(e)));
   if (const char *e = getenv("RAPID_FUSE_BSET")) c->fuse_bset = e[0] == '1';
   if (const char *e = getenv("RAPID_BSET_PARENT")) c->bset_parent = e[0] != '0';
@@ -1029,6 +1067,27 @@ int rapid_segment(rapid_ctx *c, const uint8_t *image, int32_t H, int32_t W, cons
       if ((rc = cuda_check(c, e, "end capture"))) {
         drop_events();
         return rc;
+      }
+      if (c->l2_persist) {  // the capture stream's window, set on every kernel node explicitly
+        cudaStreamAttrValue sv{};
+        if (cudaStreamGetAttribute(c->cap_stream, cudaStreamAttributeAccessPolicyWindow, &sv) == cudaSuccess &&
+            sv.accessPolicyWindow.num_bytes > 0) {
+          size_t nn = 0;
+          cudaGraphGetNodes(g, nullptr, &nn);
+          std::vector<cudaGraphNode_t> nodes(nn);
+          if (nn) cudaGraphGetNodes(g, nodes.data(), &nn);
+          cudaKernelNodeAttrValue kv{};
+          kv.accessPolicyWindow = sv.accessPolicyWindow;
+          int nk = 0;
+          for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType t;
+            if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel &&
+                cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &kv) == cudaSuccess)
+              nk++;
+          }
+          if (getenv("RAPID_VERBOSE")) fprintf(stderr, "rapid: access-policy window on %d kernel nodes\n", nk);
+        }
+        cudaGetLastError();
       }
       rapid_ctx::GraphEntry ne;
       const cudaError_t ei = cudaGraphInstantiate(&ne.exec, g, 0);

@@ -88,6 +88,12 @@ struct SpDev {
   int32_t *out;              // [K] rem: outflow budget left in the current phase (O6', A19)
   uint32_t *dirty;           // byte map [K] (as words): superpixels whose sums (or budget) changed this phase
   int32_t *remap;            // [K]
+  // K5's packed per-phase stats deltas: [K][4] u64, three words of two signed 32-bit fields
+  // {n, r}, {g, b}, {x, y} (two's complement, summed modulo 2^64), folded into sums by K3 and
+  // zero outside a phase; used while every snapshot size is <= the stage's limit
+  unsigned long long *dsum;   // null: K5 always updates the sums directly
+  unsigned int *big;          // set by K3 once a snapshot size exceeds nlim (sticky for the call)
+  int32_t nlim;               // the call's size limit: the smallest stage limit
 };
 
 struct RecV {
@@ -264,8 +270,29 @@ __device__ __forceinline__ void mark_dirty(uint32_t *dirty, int key) {
   reinterpret_cast<uint8_t *>(dirty)[key] = 1u;  // byte map: a plain store, no atomic
 }
 
+// One aggregated stats delta: six int64 REDs on the sums, or (dsum) three on the packed
+// per-phase delta words {n, r}, {g, b}, {x, y} — lo + hi * 2^32 modulo 2^64, so that negation
+// and every sum of packed words stay packed; exact while each field's phase total fits int32
+__device__ __forceinline__ void red_sums(const long long tot[6], int key, bool negate,
+                                         unsigned long long *sums, unsigned long long *dsum) {
+  if (dsum != nullptr) {
+    unsigned long long *q = dsum + (size_t)key * 4;
+#pragma unroll
+    for (int w = 0; w < 3; w++) {
+      const unsigned long long v =
+          (unsigned long long)tot[2 * w] + ((unsigned long long)tot[2 * w + 1] << 32);
+      red_add_keep(&q[w], negate ? 0ull - v : v);
+    }
+  } else {
+    unsigned long long *q = sums + (size_t)key * SUMW;
+#pragma unroll
+    for (int f = 0; f < 6; f++) red_add_keep(&q[f], (unsigned long long)(negate ? -tot[f] : tot[f]));
+  }
+}
+
 __device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[6], bool negate,
-                                         unsigned long long *sums, uint32_t *dirty) {
+                                         unsigned long long *sums, uint32_t *dirty,
+                                         unsigned long long *dsum = nullptr) {
   if (__ballot_sync(FULL, valid) == 0u) return;  // warp-uniform
   const WarpRun run = warp_runs(valid, key);
   const int lane = lane_id();
@@ -285,9 +312,7 @@ __device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[
   }
   if (valid && run.end) {
     const long long tot[6] = {(long long)v0, (long long)v1, (long long)v2, (long long)v3, v4, v5};
-    unsigned long long *s = sums + (size_t)key * SUMW;
-#pragma unroll
-    for (int f = 0; f < 6; f++) red_add_keep(&s[f], (unsigned long long)(negate ? -tot[f] : tot[f]));
+    red_sums(tot, key, negate, sums, dsum);
     if (dirty != nullptr) mark_dirty(dirty, key);
   }
 }
@@ -297,7 +322,8 @@ __device__ __forceinline__ void agg_sums(bool valid, int key, const long long d[
 // <= 16 x 32), colour sums (18 bits each; <= 255 x 16 x 32), position sums (26 bits each;
 // <= 2^20 x 32) — so the segmented scan moves 2 words instead of 6.
 __device__ __forceinline__ void agg_sums_small(bool valid, int key, const long long d[6], bool negate,
-                                               unsigned long long *sums, uint32_t *dirty) {
+                                               unsigned long long *sums, uint32_t *dirty,
+                                               unsigned long long *dsum = nullptr) {
   if (__ballot_sync(FULL, valid) == 0u) return;  // warp-uniform
   const int lane = lane_id();
   unsigned long long u0 = 0, u1 = 0;
@@ -337,9 +363,7 @@ __device__ __forceinline__ void agg_sums_small(bool valid, int key, const long l
     const long long tot[6] = {(long long)(u0 & 0x3FFull), (long long)((u0 >> 10) & 0x3FFFFull),
                               (long long)((u0 >> 28) & 0x3FFFFull), (long long)(u0 >> 46),
                               (long long)(u1 & 0x3FFFFFFull), (long long)(u1 >> 26)};
-    unsigned long long *s = sums + (size_t)key * SUMW;
-#pragma unroll
-    for (int f = 0; f < 6; f++) red_add_keep(&s[f], (unsigned long long)(negate ? -tot[f] : tot[f]));
+    red_sums(tot, key, negate, sums, dsum);
     if (dirty != nullptr) mark_dirty(dirty, key);
   }
 }

@@ -216,7 +216,27 @@ __device__ __forceinline__ Rec make_rec(const SpDev &sp, int k, bool full = true
   // kernel reads sums its own atomics wrote
   const ulonglong2 s01 = ld64_v2u64(sp.sums + (size_t)k * SUMW), s23 = ld64_v2u64(sp.sums + (size_t)k * SUMW + 2);
   const ulonglong2 s45 = ld64_v2u64(sp.sums + (size_t)k * SUMW + 4);
-  const unsigned long long s[6] = {s01.x, s01.y, s23.x, s23.y, s45.x, s45.y};
+  unsigned long long s[6] = {s01.x, s01.y, s23.x, s23.y, s45.x, s45.y};
+  if (sp.dsum != nullptr) {  // fold K5's packed deltas of the last phase into the sums and clear them
+    unsigned long long *q = sp.dsum + (size_t)k * 4;
+    const ulonglong2 e01 = ld64_v2u64(q), e2 = ld64_v2u64(q + 2);
+    if ((e01.x | e01.y | e2.x) != 0ull) {
+      const unsigned long long e[3] = {e01.x, e01.y, e2.x};
+#pragma unroll
+      for (int w = 0; w < 3; w++) {
+        const long long lo = (long long)(int32_t)(uint32_t)e[w];
+        const long long hi = (long long)(e[w] - (unsigned long long)lo) >> 32;
+        s[2 * w] += (unsigned long long)lo;
+        s[2 * w + 1] += (unsigned long long)hi;
+      }
+      unsigned long long *t = sp.sums + (size_t)k * SUMW;
+      *reinterpret_cast<ulonglong2 *>(t) = make_ulonglong2(s[0], s[1]);
+      *reinterpret_cast<ulonglong2 *>(t + 2) = make_ulonglong2(s[2], s[3]);
+      *reinterpret_cast<ulonglong2 *>(t + 4) = make_ulonglong2(s[4], s[5]);
+      *reinterpret_cast<ulonglong2 *>(q) = make_ulonglong2(0ull, 0ull);
+      q[2] = 0ull;
+    }
+  }
   const unsigned long long n = s[0];
   Rec r;
   r.n = (int32_t)n;
@@ -337,6 +357,10 @@ __device__ __forceinline__ void snapshot_warps(const SnapArgs &a, int wid, int n
         // the outflow budget of the next phase starts full: every superpixel whose rem[] the
         // last phase lowered (every proposal's source) was marked dirty by K4 or K5
         a.sp.out[k] = outflow_budget(r, a.l_num, a.l_den);
+        // K5's packed-delta condition: flag (plain store, sticky for the call) any snapshot size
+        // above the call's limit; every record written since the call's first (full) refresh
+        // went through here
+        if (r.n > a.sp.nlim) *a.sp.big = 1u;
       }
     }
   }

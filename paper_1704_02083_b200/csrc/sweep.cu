@@ -1029,6 +1029,9 @@ __global__ void __launch_bounds__(256, 8) k_commit(const PhaseArgs a) {  // 8 CT
   pdl_wait_and_trigger();
   const unsigned long long n = cta_count(a.prev, a.prop_count, !SNAP);
   if (n == 0) return;  // SNAP: grid-uniform (an empty list marks nothing to refresh)
+  // packed deltas (3 REDs per aggregated run instead of 6) while every snapshot size is within
+  // the stage's limit: then no field of a superpixel's phase total leaves int32
+  unsigned long long *const ds = (a.sp.dsum != nullptr && *a.sp.big == 0u) ? a.sp.dsum : nullptr;
   unsigned c_commit = 0, c_rej = 0;
   for (unsigned long long base = blockIdx.x * 256ull; base < n; base += gridDim.x * 256ull) {
     const unsigned long long i = base + threadIdx.x;
@@ -1064,11 +1067,11 @@ __global__ void __launch_bounds__(256, 8) k_commit(const PhaseArgs a) {  // 8 CT
     }
     if (a.size_mode == 2 && __ballot_sync(FULL, rej) && lane_id() == 0) *a.victim_any = 1u;  // once per warp
     if (PIXEL || a.st.b <= 4) {  // warp-uniform
-      agg_sums_small(ok, kb + A, d, true, a.sp.sums, a.sp.dirty);
-      agg_sums_small(ok, kb + B, d, false, a.sp.sums, a.sp.dirty);
+      agg_sums_small(ok, kb + A, d, true, a.sp.sums, a.sp.dirty, ds);
+      agg_sums_small(ok, kb + B, d, false, a.sp.sums, a.sp.dirty, ds);
     } else {
-      agg_sums(ok, kb + A, d, true, a.sp.sums, a.sp.dirty);
-      agg_sums(ok, kb + B, d, false, a.sp.sums, a.sp.dirty);
+      agg_sums(ok, kb + A, d, true, a.sp.sums, a.sp.dirty, ds);
+      agg_sums(ok, kb + B, d, false, a.sp.sums, a.sp.dirty, ds);
     }
     c_commit += __popc(__ballot_sync(FULL, ok));
     c_rej += __popc(__ballot_sync(FULL, rej));

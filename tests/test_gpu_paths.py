@@ -33,7 +33,7 @@ def make_ctx(env, pixels, sps):
 VARIANTS = [{}, {"RAPID_NO_GRAPH": "1"}, {"RAPID_SWEEP": "scan"}, {"RAPID_FUSE_BSET": "1"}, {"RAPID_FUSE_SNAP": "1"},
             {"RAPID_NO_TMA": "1"}, {"RAPID_BSET_PARENT": "0"}, {"RAPID_SWEEP_NO_SMALLB": "1"},
             {"RAPID_PDL": "1"}, {"RAPID_ADJ": "tma"}, {"RAPID_BSET_ROWS": "0"},
-            {"RAPID_BSET_ROWS": "2"}]
+            {"RAPID_BSET_ROWS": "2"}, {"RAPID_PACKED": "0"}]
 
 
 @pytest.mark.parametrize("cfg,side", [(2, 1024), (4, 1024), (5, 0)])
@@ -219,6 +219,20 @@ def test_random_cases_through_64bit_block_variant():
     r = make_ctx({"RAPID_SWEEP_NO_SMALLB": "1"}, 1 << 22, 1 << 16)
     try:
         random_all_options(r, 77, 16)
+    finally:
+        r.close()
+
+
+@pytest.mark.parametrize("lim", [60, 150, 600])
+def test_random_cases_packed_delta_switch(lim):
+    """K5 packs its stats deltas (3 REDs per run, folded by K3) only while every snapshot size
+    is within the stage's limit; RAPID_PACKED_LIM caps that limit near the random cases'
+    superpixel sizes so that calls run packed, direct, or switch to direct once merges grow a
+    superpixel past it: bit-exact with the oracle in every case."""
+    from test_gpu_parity import random_all_options
+    r = make_ctx({"RAPID_PACKED_LIM": str(lim)}, 1 << 22, 1 << 16)
+    try:
+        random_all_options(r, 91 + lim, 12)
     finally:
         r.close()
 

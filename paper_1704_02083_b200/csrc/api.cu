@@ -28,6 +28,7 @@ struct Ctl {  // per-segmentation device control block (zeroed at the start of e
   unsigned int vtotal, deg_total, npairs, atotal;
   unsigned int mflag[2];  // cooperative merge match: pending flags per round parity
   unsigned int wq[MAXS * MAXSW * 4];  // k_sweep work-queue counters, one per phase
+  unsigned int list_count[MAXS * MAXSW * 4];  // k_bset_list: candidate-list lengths, one per phase
   unsigned int big;  // K3: some snapshot size exceeded the call's packed-delta limit (K5 then REDs the sums)
 };
 
@@ -103,8 +104,10 @@ struct rapid_ctx {
   int scan_grid = 0, eval_grid = 0, sweep_grid = 0, tiles_grid = 0;  // persistent grid sizes (CTAs)
   int sweep_tail = 25;  // RAPID_SWEEP_TAIL: % of K4's words dealt in quarter-size groups at the end (block stages)
   int sweep_gpw = 2;  // K4 word groups per warp (RAPID_SWEEP_GPW overrides, A/B testing)
+  int sweep_list_minb = 0;  // RAPID_SWEEP_LIST=b: block stages with blocks >= b take the per-phase candidate list (0: off)
   int snap_ctas = 4;  // RAPID_SNAP_CTAS: K3 CTAs per SM
   bool packed = true;  // RAPID_PACKED=0: K5 always issues the six int64 REDs per run on the sums
+  bool packed_force = false;  // RAPID_PACKED=1: packed deltas below the size crossover too (tests)
   int packed_lim = 0;  // RAPID_PACKED_LIM=n (> 0): caps the stages' size limits (tests the per-phase switch)
   bool fuse_snap = false;  // RAPID_FUSE_SNAP=1: K3 of the next phase runs at the end of a cooperative K5 (measured: same step time)
   bool bset_parent = true;  // dyadic stages: boundary sets from the parent map (RAPID_BSET_PARENT=0: child-map tile pass)
@@ -545,7 +548,11 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
     for (int st = 0; st < (int)P.nst; st++) lim = std::min(lim, (int)P.st[st].maxn_lim);
     if (c->packed_lim > 0) lim = std::min(lim, c->packed_lim);
     sp.nlim = lim;
-    if (!c->packed || lim <= 0) sp.dsum = nullptr;
+    // measured crossover: the fold in K3 costs about what the halved REDs save in K5 below a few
+    // hundred Mpx per call (configs 2, 3, 5: packed 2.78 / 4.14 vs direct 2.67 / 4.13 ms), while
+    // config 4 (1.07 Gpx) gains 0.16 ms; RAPID_PACKED=1 forces packing at any size
+    const bool big_call = (uint64_t)P.B * (uint64_t)P.H * (uint64_t)P.W >= (1ull << 28);
+    if (!c->packed || lim <= 0 || (!big_call && !c->packed_force)) sp.dsum = nullptr;
   }
   const int32_t *T = (const int32_t *)c->tab.p;
 
@@ -693,6 +700,8 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           pa.gating = gating;
           pa.bset = c->use_bset ? (uint32_t *)c->bset.p : nullptr;
           pa.wq = &ctl->wq[g];
+          pa.list = (uint32_t *)c->cands.p;  // (the full-scan path's buffer; at least the phase's blocks)
+          pa.list_count = &ctl->list_count[g];
           pa.gpw = c->sweep_gpw;
           pa.tail_pct = pixel ? 0 : c->sweep_tail;  // measured: helps the latency-bound block stages only
           pa.size_mode = (int)p->size_mode;
@@ -711,8 +720,9 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
           pa.victim_any = &ctl->victim_any[st];
           if (c->use_bset) {
             Timer t2(c, s, RAPID_K_PROPOSE, st);
-            launch_sweep(pa, pixel, P.st[st].smallb, c->sm_count, s);
-            c->launches++;
+            const bool list = c->sweep_list_minb > 0 && P.st[st].b >= c->sweep_list_minb;
+            launch_sweep(pa, pixel, P.st[st].smallb, list, c->sm_count, s);
+            c->launches += list && !pixel ? 2 : 1;
           } else {
             {
               Timer t2(c, s, RAPID_K_PROPOSE, st);
@@ -948,7 +958,11 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   c->eval_grid = c->sm_count * eval_occupancy();
   c->sweep_grid = c->sm_count * sweep_occupancy();
   if (const char *e = getenv("RAPID_SWEEP_GPW")) c->sweep_gpw = std::max(1, atoi(e));
-  if (const char *e = getenv("RAPID_PACKED")) c->packed = e[0] != '0';
+  if (const char *e = getenv("RAPID_SWEEP_LIST")) c->sweep_list_minb = std::max(0, atoi(e));
+  if (const char *e = getenv("RAPID_PACKED")) {
+    c->packed = e[0] != '0';
+    c->packed_force = e[0] == '1';
+  }
   if (const char *e = getenv("RAPID_SNAP_CTAS")) c->snap_ctas = std::min(8, std::max(1, atoi(e)));
   if (const char *e = getenv("RAPID_PACKED_LIM")) c->packed_lim = std::max(0, atoi(e));
   if (const char *e = getenv("RAPID_SWEEP_TAIL")) c->sweep_tail = std::min(100, std::max(0, atoi(e)));

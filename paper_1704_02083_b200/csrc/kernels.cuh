@@ -29,6 +29,8 @@ struct PhaseArgs {
   int32_t gpw;               // k_sweep: word groups per warp to aim for (sizes the groups)
   int32_t tail_pct;          // k_sweep: % of the words dealt in quarter-size groups at the end
   unsigned int *wq;          // k_sweep: work-queue counter of this phase (zeroed per call)
+  uint32_t *list;            // k_bset_list -> k_sweep<LIST>: the phase's set bits (word << 5 | bit)
+  unsigned int *list_count;  // their number (zeroed per call)
 };
 
 struct SnapArgs {
@@ -394,7 +396,8 @@ void launch_commit(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s);
 cudaError_t launch_commit_snap(const PhaseArgs &a, bool pixel, int sm_count, cudaStream_t s);
 // boundary-set sweep: K4 build (once per stage) and the fused bitset-driven sweep
 void launch_bset_build(const PhaseArgs &a, const void *tmap, int grid, cudaStream_t s);
-void launch_sweep(const PhaseArgs &a, bool pixel, bool smallb, int sm_count, cudaStream_t s);
+// list: a block stage's per-phase candidate list (k_bset_list, then k_sweep<LIST>)
+void launch_sweep(const PhaseArgs &a, bool pixel, bool smallb, bool list, int sm_count, cudaStream_t s);
 int sweep_occupancy();
 int scan_occupancy();
 int eval_occupancy();

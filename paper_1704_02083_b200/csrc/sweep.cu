@@ -721,7 +721,7 @@ __device__ __forceinline__ i128 energy(const Rec &ra, const int4 rb, const int d
 // tiles; lane l loads bset word (tile l/8, colour c, plane row l%8), the set bits are
 // distributed 32 at a time over the lanes, and every lane re-tests its block from the label
 // map (boundary, static gate, simple point, Eq. 7), then evaluates Eqs. 1-3 as K4b does.
-template <bool PIXEL, bool GATED, int MINB, bool SMALLB = false>
+template <bool PIXEL, bool GATED, int MINB, bool SMALLB = false, bool LIST = false>
 __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) {
   pdl_wait_and_trigger();
   if (sweep_skipped(a.prev)) return;
@@ -755,55 +755,17 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
   unsigned long long pbase = 0;  // this warp's reserved proposal slots
   int pleft = 0;
   unsigned r_cand = 0, r_topo = 0, r_prop = 0, r_srej = 0, r_commit = 0;  // this warp's counters
-  // dynamic distribution of the word groups (one returned atomic per group and warp): the
-  // per-group work varies with the boundary density, static striding left a 10 % tail
-  for (unsigned g = 0;;) {
-    if (lane == 0) g = atomicAdd(a.wq, 1u);
-    g = __shfl_sync(FULL, g, 0);
-    if (g >= ngroups) break;
-    // ---- this lane's word
-    const unsigned gsz = g < nhead ? G : Gt;
-    const unsigned q = (g < nhead ? g * G : head_words + (g - nhead) * Gt) + (unsigned)lane, w = q >> 3;  // (tile slot, plane row q % 8)
-    uint32_t word = 0, wpos = 0, widx = 0;
-    int wimg = 0;
-    if ((unsigned)lane < gsz && w < ntiles) {
-      const uint32_t t = a.worklist ? (uint32_t)a.worklist[w] : w;
-      const uint32_t rr = fdiv(t, st.fd_tx), img = fdiv(rr, st.fd_ty);
-      const int gx0 = (int)(t - rr * (uint32_t)st.tiles_x) * TX, gy0 = (int)(rr - img * (uint32_t)st.tiles_y) * TY;
-      widx = t * BSET_WORDS_PER_TILE + (uint32_t)(colour * (TY / 2) + (q & 7));
-      word = ld64_u32(a.bset + widx);  // 64-B fill: the phase needs 32 B of the tile's 128
-      wpos = (uint32_t)(gx0 + a.cx) | ((uint32_t)(gy0 + 2 * (q & 7) + a.cy) << 16);
-      wimg = (int)img;
-    }
-    const unsigned cw = __popc(word);
-    unsigned incl = cw;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned v = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const unsigned total = __shfl_sync(FULL, incl, 31);
-    for (unsigned rb = 0; rb < total; rb += 32) {
-      const unsigned k = rb + lane;
-      int j = 0;  // the lane whose word holds candidate k: #lanes with incl <= k
-#pragma unroll
-      for (int h = 16; h > 0; h >>= 1) {
-        const unsigned v = __shfl_sync(FULL, incl, j + h - 1);
-        if (v <= k) j += h;
-      }
-      const uint32_t wj = __shfl_sync(FULL, word, j);
-      const unsigned ej = __shfl_sync(FULL, incl, j) - __popc(wj);
-      const uint32_t pj = __shfl_sync(FULL, wpos, j);
-      const uint32_t xj = __shfl_sync(FULL, widx, j);
-      const int img = __shfl_sync(FULL, wimg, j);
-      const bool have = k < total;
+  // one round: every lane tests (have) the block of bit r of word wj (bit 0 of a one-bit word in
+  // LIST mode) at plane position pj = (x of bit 0) | (y << 16) and evaluates it (Eqs. 1-3)
+  auto round = [&](const bool have, const int img, const uint32_t xj, const uint32_t wj, const unsigned r,
+                   const uint32_t pj) {
       bool cand = false, emit = false, prop = false, srej = false;
       int A = 0, Bm = 0, kb = img * a.M, gx = 0, gy = 0;
       unsigned ins = 0;
       uint32_t rgb = 0;
       int d[6] = {0, 0, 0, 0, 0, 0};  // block data: n, colour sums, position sums (all < 2^31)
       if (have) {
-        const unsigned bit = nth_set_bit(wj, k - ej);
+        const unsigned bit = nth_set_bit(wj, r);
         gx = (int)(pj & 0xffffu) + 2 * (int)bit;
         gy = (int)(pj >> 16);
         // block data depends on the position only: issued together with the window loads
@@ -1000,7 +962,75 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
           pleft -= np;
         }
       }
+  };
+  auto deal_groups = [&]() {
+  // dynamic distribution of the word groups (one returned atomic per group and warp): the
+  // per-group work varies with the boundary density, static striding left a 10 % tail
+  for (unsigned g = 0;;) {
+    if (lane == 0) g = atomicAdd(a.wq, 1u);
+    g = __shfl_sync(FULL, g, 0);
+    if (g >= ngroups) break;
+    // ---- this lane's word
+    const unsigned gsz = g < nhead ? G : Gt;
+    const unsigned q = (g < nhead ? g * G : head_words + (g - nhead) * Gt) + (unsigned)lane, w = q >> 3;  // (tile slot, plane row q % 8)
+    uint32_t word = 0, wpos = 0, widx = 0;
+    int wimg = 0;
+    if ((unsigned)lane < gsz && w < ntiles) {
+      const uint32_t t = a.worklist ? (uint32_t)a.worklist[w] : w;
+      const uint32_t rr = fdiv(t, st.fd_tx), img = fdiv(rr, st.fd_ty);
+      const int gx0 = (int)(t - rr * (uint32_t)st.tiles_x) * TX, gy0 = (int)(rr - img * (uint32_t)st.tiles_y) * TY;
+      widx = t * BSET_WORDS_PER_TILE + (uint32_t)(colour * (TY / 2) + (q & 7));
+      word = ld64_u32(a.bset + widx);  // 64-B fill: the phase needs 32 B of the tile's 128
+      wpos = (uint32_t)(gx0 + a.cx) | ((uint32_t)(gy0 + 2 * (q & 7) + a.cy) << 16);
+      wimg = (int)img;
     }
+    const unsigned cw = __popc(word);
+    unsigned incl = cw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const unsigned total = __shfl_sync(FULL, incl, 31);
+    for (unsigned rb = 0; rb < total; rb += 32) {
+      const unsigned k = rb + lane;
+      int j = 0;  // the lane whose word holds candidate k: #lanes with incl <= k
+#pragma unroll
+      for (int h = 16; h > 0; h >>= 1) {
+        const unsigned v = __shfl_sync(FULL, incl, j + h - 1);
+        if (v <= k) j += h;
+      }
+      const uint32_t wj = __shfl_sync(FULL, word, j);
+      const unsigned ej = __shfl_sync(FULL, incl, j) - __popc(wj);
+      const uint32_t pj = __shfl_sync(FULL, wpos, j);
+      const uint32_t xj = __shfl_sync(FULL, widx, j);
+      const int img = __shfl_sync(FULL, wimg, j);
+      round(k < total, img, xj, wj, k - ej, pj);
+    }
+  }
+  };
+  if constexpr (LIST) {
+    // the phase's set bits compacted into a.list by k_bset_list (one entry per bit: word index
+    // << 5 | bit): every round is 32 candidates, no dealing; static striding (the rounds cost
+    // about the same)
+    const unsigned n = *a.list_count;
+    for (unsigned base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u; base < n; base += nw * 32u) {
+      const unsigned i = base + (unsigned)lane;
+      uint32_t e = 0, xj = 0, pj = 0;
+      int img = 0;
+      if (i < n) {
+        e = a.list[i];
+        xj = e >> 5;
+        const uint32_t t = xj / BSET_WORDS_PER_TILE, q = xj & 7u;
+        const uint32_t rr = fdiv(t, st.fd_tx), im = fdiv(rr, st.fd_ty);
+        const int gx0 = (int)(t - rr * (uint32_t)st.tiles_x) * TX, gy0 = (int)(rr - im * (uint32_t)st.tiles_y) * TY;
+        pj = (uint32_t)(gx0 + a.cx) | ((uint32_t)(gy0 + 2 * (int)q + a.cy) << 16);
+        img = (int)im;
+      }
+      round(i < n, img, xj, 1u << (e & 31u), 0u, pj);
+    }
+  } else {
+    deal_groups();
   }
   if (GATED) {
     if (lane < pleft) a.props[pbase + lane] = make_uint4(0u, 0xffffffffu, 0u, 0u);
@@ -1015,6 +1045,46 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
   }
   __syncthreads();
   if (threadIdx.x < 5 && s_cnt[threadIdx.x]) atomicAdd(&a.cnt[threadIdx.x], (unsigned long long)s_cnt[threadIdx.x]);
+}
+
+// Per-phase candidate list of a block stage (k_sweep's LIST mode): every set bit of the phase
+// colour's boundary-set words of the worklist tiles as (word index << 5 | bit), compacted with
+// one returned atomic per warp.  The order is irrelevant: K4's decisions, K5's all-or-nothing
+// budgets and the integer atomics do not depend on it.
+__global__ void __launch_bounds__(256) k_bset_list(const PhaseArgs a) {
+  pdl_wait_and_trigger();
+  if (sweep_skipped(a.prev)) return;
+  const StageDev &st = a.st;
+  const unsigned ntiles = a.worklist ? *a.nwork : (unsigned)(st.tiles_x * st.tiles_y) * (unsigned)a.B;
+  const unsigned nwords = ntiles * (TY / 2);
+  const int colour = a.cx | (a.cy << 1);
+  const int lane = lane_id();
+  for (unsigned base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; base < nwords; base += gridDim.x * blockDim.x) {
+    const unsigned q = base + (unsigned)lane;
+    uint32_t word = 0, widx = 0;
+    if (q < nwords) {
+      const unsigned w = q >> 3;
+      const uint32_t t = a.worklist ? (uint32_t)a.worklist[w] : w;
+      widx = t * BSET_WORDS_PER_TILE + (uint32_t)(colour * (TY / 2) + (q & 7));
+      word = a.bset[widx];
+    }
+    unsigned incl = __popc(word);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const unsigned total = __shfl_sync(FULL, incl, 31);
+    if (total == 0u) continue;  // warp-uniform
+    unsigned off = 0;
+    if (lane == 31) off = atomicAdd(a.list_count, total);
+    off = __shfl_sync(FULL, off, 31) + incl - __popc(word);
+    while (word) {
+      const uint32_t b = (uint32_t)__ffs(word) - 1u;
+      word &= word - 1u;
+      a.list[off++] = (widx << 5) | b;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ K5: commit
@@ -1194,15 +1264,21 @@ bool launch_merge_adjacency_tma(const MergeArgs &m, const void *tmap, int grid, 
   return true;
 }
 
-void launch_sweep(const PhaseArgs &a, bool pixel, bool smallb, int sm_count, cudaStream_t s) {
+void launch_sweep(const PhaseArgs &a, bool pixel, bool smallb, bool list, int sm_count, cudaStream_t s) {
   const bool gated = a.size_mode != 0;
   static int occ[5] = {0, 0, 0, 0, 0};
   const int mb = g_sweep_minb ? g_sweep_minb : (pixel ? 4 : smallb ? g_sweep_minb_small : 3);
   if (!occ[mb]) occ[mb] = mb == 2 ? sweep_occ<2>() : mb == 3 ? sweep_occ<3>() : sweep_occ<4>();
   const int grid = sm_count * occ[mb];
+  list = list && !pixel;
+  if (list) launch_pdl(k_bset_list, dim3(sm_count * 8), dim3(256), s, a);
 #define RAPID_SWEEP_LAUNCH(MB)                                                                     \
   if (pixel && gated) launch_pdl(k_sweep<true, true, MB>, dim3(grid), dim3(K4B_THREADS), s, a);        \
   else if (pixel) launch_pdl(k_sweep<true, false, MB>, dim3(grid), dim3(K4B_THREADS), s, a);           \
+  else if (list && gated && smallb) launch_pdl(k_sweep<false, true, MB, true, true>, dim3(grid), dim3(K4B_THREADS), s, a); \
+  else if (list && smallb) launch_pdl(k_sweep<false, false, MB, true, true>, dim3(grid), dim3(K4B_THREADS), s, a); \
+  else if (list && gated) launch_pdl(k_sweep<false, true, MB, false, true>, dim3(grid), dim3(K4B_THREADS), s, a); \
+  else if (list) launch_pdl(k_sweep<false, false, MB, false, true>, dim3(grid), dim3(K4B_THREADS), s, a); \
   else if (gated && smallb) launch_pdl(k_sweep<false, true, MB, true>, dim3(grid), dim3(K4B_THREADS), s, a); \
   else if (smallb) launch_pdl(k_sweep<false, false, MB, true>, dim3(grid), dim3(K4B_THREADS), s, a);   \
   else if (gated) launch_pdl(k_sweep<false, true, MB>, dim3(grid), dim3(K4B_THREADS), s, a);           \

@@ -33,7 +33,8 @@ def make_ctx(env, pixels, sps):
 VARIANTS = [{}, {"RAPID_NO_GRAPH": "1"}, {"RAPID_SWEEP": "scan"}, {"RAPID_FUSE_BSET": "1"}, {"RAPID_FUSE_SNAP": "1"},
             {"RAPID_NO_TMA": "1"}, {"RAPID_BSET_PARENT": "0"}, {"RAPID_SWEEP_NO_SMALLB": "1"},
             {"RAPID_PDL": "1"}, {"RAPID_ADJ": "tma"}, {"RAPID_BSET_ROWS": "0"},
-            {"RAPID_BSET_ROWS": "2"}, {"RAPID_PACKED": "0"}]
+            {"RAPID_BSET_ROWS": "2"}, {"RAPID_PACKED": "1"},
+            {"RAPID_SWEEP_LIST": "2"}]
 
 
 @pytest.mark.parametrize("cfg,side", [(2, 1024), (4, 1024), (5, 0)])
@@ -223,14 +224,28 @@ def test_random_cases_through_64bit_block_variant():
         r.close()
 
 
+def test_random_cases_through_candidate_list():
+    """The randomized all-options sweep with every block stage (b >= 2) evaluated from the
+    per-phase candidate list (RAPID_SWEEP_LIST=2: k_bset_list + k_sweep<LIST>), once with the
+    64-bit position-factor variant too: bit-exact with the oracle."""
+    from test_gpu_parity import random_all_options
+    for env, seed in (({"RAPID_SWEEP_LIST": "2"}, 53), ({"RAPID_SWEEP_LIST": "2", "RAPID_SWEEP_NO_SMALLB": "1"}, 54)):
+        r = make_ctx(env, 1 << 22, 1 << 16)
+        try:
+            random_all_options(r, seed, 12)
+        finally:
+            r.close()
+
+
 @pytest.mark.parametrize("lim", [60, 150, 600])
 def test_random_cases_packed_delta_switch(lim):
     """K5 packs its stats deltas (3 REDs per run, folded by K3) only while every snapshot size
     is within the stage's limit; RAPID_PACKED_LIM caps that limit near the random cases'
     superpixel sizes so that calls run packed, direct, or switch to direct once merges grow a
-    superpixel past it: bit-exact with the oracle in every case."""
+    superpixel past it: bit-exact with the oracle in every case.  (Calls this small take the
+    direct REDs by default; RAPID_PACKED=1 forces the packed path.)"""
     from test_gpu_parity import random_all_options
-    r = make_ctx({"RAPID_PACKED_LIM": str(lim)}, 1 << 22, 1 << 16)
+    r = make_ctx({"RAPID_PACKED": "1", "RAPID_PACKED_LIM": str(lim)}, 1 << 22, 1 << 16)
     try:
         random_all_options(r, 91 + lim, 12)
     finally:

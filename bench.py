@@ -268,6 +268,59 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ----------------------------------------------------------------------------- host link bound
+def link_bound(h2d_bytes, d2h_bytes, dev_ms_total, steps, e2e_ms, stream):
+    """What bounds the end-to-end number: the host link, measured here with pinned copies of
+    1 GiB (best of 3; H2D alone, D2H alone, both at once on two streams), and the pipeline of
+    rapid_segment_host_stream over K steps — the first image's copy-in and the last step's
+    labels' copy-out cannot overlap anything, every other step costs the slowest of its
+    copy-in, its copy-out, both copies through the duplex link, and its segmentation:
+        T(K) = t_h2d + t_seg + (K - 1) * max(t_h2d, t_d2h, t_both, t_seg) + t_d2h
+    with t_both = (bytes in + bytes out) / duplex bandwidth."""
+    import torch
+    n = 1 << 30
+    hs = torch.empty(n, dtype=torch.uint8).pin_memory()
+    hd = torch.empty(n, dtype=torch.uint8).pin_memory()
+    da = torch.empty(n, dtype=torch.uint8, device="cuda")
+    db = torch.empty(n, dtype=torch.uint8, device="cuda")
+    s2 = torch.cuda.Stream()
+
+    def timed(fn, streams):
+        best = None
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            for st in streams:
+                st.synchronize()
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        return best
+
+    with torch.cuda.stream(stream):
+        t_in = timed(lambda: da.copy_(hs, non_blocking=True), [stream])
+        t_out = timed(lambda: hd.copy_(db, non_blocking=True), [stream])
+
+        def both():
+            da.copy_(hs, non_blocking=True)
+            with torch.cuda.stream(s2):
+                hd.copy_(db, non_blocking=True)
+        t_both = timed(both, [stream, s2])
+    del hs, hd, da, db
+    gb = n / 1e9
+    h2d, d2h, duplex = gb / t_in, gb / t_out, 2 * gb / t_both  # GB/s
+    t_h2d, t_d2h = h2d_bytes / 1e9 / h2d, d2h_bytes / 1e9 / d2h
+    t_both = (h2d_bytes + d2h_bytes) / 1e9 / duplex
+    t_seg = dev_ms_total / steps / 1e3
+    T = t_h2d + t_seg + (steps - 1) * max(t_h2d, t_d2h, t_both, t_seg) + t_d2h
+    return {"h2d_gbs": round(h2d, 2), "d2h_gbs": round(d2h, 2), "duplex_gbs": round(duplex, 2),
+            "model_ms": round(T * 1e3, 2), "measured_ms": round(e2e_ms, 2),
+            "frac": round(T * 1e3 / e2e_ms, 4),
+            "how": "pinned 1 GiB torch copies, best of 3 (H2D, D2H, both on two streams); "
+                   "T(K) = t_h2d + t_seg + (K-1) max(t_h2d, t_d2h, (in + out) / duplex, t_seg) + t_d2h; "
+                   "frac = T(K) / measured"}
+
+
 # ----------------------------------------------------------------------------- algorithmic bytes
 def phase_bytes(info, w, window):
     """SURVEY §8(d) model per K4 launch: 4 B x window blocks + c_s x candidates needing colour
@@ -384,6 +437,7 @@ def run_ours(args):
                "unit": "Mpixel/s", "h2d_bytes_per_step": w.pixels * 3, "d2h_bytes_per_step": w.pixels * 4,
                "api": "rapid_segment_host_stream (pinned host buffers; H2D, D2H and compute overlapped "
                       "across consecutive steps)"}
+        e2e["link"] = link_bound(w.pixels * 3, w.pixels * 4, ms_max, args.steps, te, stream)
         r.set_profiling(1)
 
     # segmentation quality of this step's labels against the generator's

@@ -389,8 +389,12 @@ __global__ void __launch_bounds__(256) k_merge_adjacency(const MergeArgs a) {
 // victims' boundary blocks (a victim passed the static gate); their set bits are dealt 32 at a
 // time to the lanes, each lane loads its block's label and victim flag and, for a victim block
 // only, its four neighbours, adding the shared edge lengths to the (victim, neighbour) hash.
-// Two dependent loads per set bit instead of a full pass over the stage map.
-__global__ void __launch_bounds__(256) k_merge_adj_bset(const MergeArgs a) {
+// Two dependent loads per set bit instead of a full pass over the stage map.  U rounds of 32
+// set bits are dealt at once and their label loads (then their victim-flag loads) issued
+// together: one dependent round trip per U rounds (the pass is latency-bound; the hash totals
+// and everything after them do not depend on the insertion order).
+template <int U, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_merge_adj_bset(const MergeArgs a) {
   if (*a.victim_any == 0u) return;
   const StageDev &st = a.st;
   const int nbx = st.nbx, nby = st.nby;
@@ -412,38 +416,49 @@ __global__ void __launch_bounds__(256) k_merge_adj_bset(const MergeArgs a) {
     const unsigned total = __shfl_sync(FULL, incl, 31);
     const int32_t *map = st.map + (size_t)img * nby * nbx;
     const int kb = (int)img * a.M;
-    for (unsigned rb = 0; rb < total; rb += 32) {
-      const unsigned k = rb + lane;
-      int j = 0;  // the lane whose word holds set bit k: #lanes with incl <= k
+    for (unsigned rb = 0; rb < total; rb += 32 * U) {
+      int gx[U], gy[U], la[U];
+      bool in[U], vic[U];
 #pragma unroll
-      for (int h = 16; h > 0; h >>= 1) {
-        const unsigned v = __shfl_sync(FULL, incl, j + h - 1);
-        if (v <= k) j += h;
-      }
-      const uint32_t wj = __shfl_sync(FULL, word, j);
-      const unsigned ej = __shfl_sync(FULL, incl, j) - __popc(wj);
-      int gx = 0, gy = 0, la = -1;
-      bool vic = false;
-      if (k < total) {
-        const unsigned bit = nth_set_bit(wj, k - ej);
-        gx = gx0 + 2 * (int)bit + ((j >> 3) & 1);
-        gy = gy0 + 2 * (j & 7) + (j >> 4);
-        if (gx < nbx && gy < nby) {
-          la = map[(size_t)gy * nbx + gx];
-          vic = a.sp.victim[kb + la] != 0;  // victims are rare: their neighbours only are loaded
+      for (int u = 0; u < U; u++) {
+        const unsigned k = rb + 32 * u + lane;
+        int j = 0;  // the lane whose word holds set bit k: #lanes with incl <= k
+#pragma unroll
+        for (int h = 16; h > 0; h >>= 1) {
+          const unsigned v = __shfl_sync(FULL, incl, j + h - 1);
+          if (v <= k) j += h;
+        }
+        const uint32_t wj = __shfl_sync(FULL, word, j);
+        const unsigned ej = __shfl_sync(FULL, incl, j) - __popc(wj);
+        gx[u] = 0;
+        gy[u] = 0;
+        in[u] = false;
+        if (k < total) {
+          const unsigned bit = nth_set_bit(wj, k - ej);
+          gx[u] = gx0 + 2 * (int)bit + ((j >> 3) & 1);
+          gy[u] = gy0 + 2 * (j & 7) + (j >> 4);
+          in[u] = gx[u] < nbx && gy[u] < nby;
         }
       }
-      const unsigned vm = __ballot_sync(FULL, vic);
-      if (vm == 0u) continue;  // warp-uniform
-      if (a.vtile && lane == __ffs(vm) - 1) a.vtile[tile] = a.vstamp;  // (the final remap visits marked tiles only)
-      if (!vic) continue;
-      const size_t p = (size_t)gy * nbx + gx;
-      const int nq[4] = {gy > 0 ? map[p - nbx] : la, gx + 1 < nbx ? map[p + 1] : la,
-                         gy + 1 < nby ? map[p + nbx] : la, gx > 0 ? map[p - 1] : la};
-      const unsigned ew = (unsigned)(st.xs[gx + 1] - st.xs[gx]), eh = (unsigned)(st.ys[gy + 1] - st.ys[gy]);
 #pragma unroll
-      for (int d = 0; d < 4; d++)
-        if (nq[d] != la) hash_add(a, kb + la, kb + nq[d], (d & 1) ? eh : ew);
+      for (int u = 0; u < U; u++) la[u] = in[u] ? map[(size_t)gy[u] * nbx + gx[u]] : -1;
+#pragma unroll
+      for (int u = 0; u < U; u++) vic[u] = in[u] && a.sp.victim[kb + la[u]] != 0;  // victims are rare
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const unsigned vm = __ballot_sync(FULL, vic[u]);
+        if (vm == 0u) continue;  // warp-uniform
+        if (a.vtile && lane == __ffs(vm) - 1) a.vtile[tile] = a.vstamp;  // (the final remap visits marked tiles only)
+        if (!vic[u]) continue;
+        const size_t p = (size_t)gy[u] * nbx + gx[u];
+        const int l = la[u];
+        const int nq[4] = {gy[u] > 0 ? map[p - nbx] : l, gx[u] + 1 < nbx ? map[p + 1] : l,
+                           gy[u] + 1 < nby ? map[p + nbx] : l, gx[u] > 0 ? map[p - 1] : l};
+        const unsigned ew = (unsigned)(st.xs[gx[u] + 1] - st.xs[gx[u]]), eh = (unsigned)(st.ys[gy[u] + 1] - st.ys[gy[u]]);
+#pragma unroll
+        for (int d = 0; d < 4; d++)
+          if (nq[d] != l) hash_add(a, kb + l, kb + nq[d], (d & 1) ? eh : ew);
+      }
     }
   }
 }
@@ -1507,6 +1522,8 @@ void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s) {
 }
 
 int g_bset_rows = 1;  // RAPID_BSET_ROWS=0: the warp-per-parent-row boundary-set pass (k_bset_dyadic); 2: rows everywhere
+int g_adj_minb8 = 1;  // k_merge_adj_bset at 32 registers, 8 CTAs per SM (RAPID_ADJ_MINB8=0: 39 registers, 6)
+int g_adj_ilp = 1;  // RAPID_ADJ_ILP=1/2/4: rounds of set bits whose label loads k_merge_adj_bset issues together
 int g_adj_tma = 0;  // RAPID_ADJ=tma: the victim adjacency from the TMA tile stream instead of the boundary sets
 
 cudaError_t launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, int grid, cudaStream_t s,
@@ -1519,7 +1536,18 @@ cudaError_t launch_merge_round(const MergeArgs &a, const void *tmap, int tgrid, 
   const size_t nb = (size_t)a.st.nbx * a.st.nby * a.B;
   (void)nb;
   if (a.bset && a.worklist && g_adj_tma == 0) {  // (ungated stages: dense sets, the tile stream is faster)
-    k_merge_adj_bset<<<148 * 8, 256, 0, s>>>(a);
+    // one wave of resident CTAs (the loop strides over the worklist tiles)
+    const void *fn = g_adj_ilp >= 4 ? (const void *)k_merge_adj_bset<4>
+                   : g_adj_ilp >= 2 ? (const void *)k_merge_adj_bset<2>
+                   : g_adj_minb8 ? (const void *)k_merge_adj_bset<1, 8> : (const void *)k_merge_adj_bset<1>;
+    int nbk = 0, dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbk, fn, 256, 0);
+    MergeArgs aa = a;
+    void *args[] = {&aa};
+    const cudaError_t e = cudaLaunchKernel(fn, dim3(sms * std::max(1, std::min(nbk, 8))), dim3(256), args, 0, s);
+    if (e != cudaSuccess) return e;
   }
   else if (!launch_merge_adjacency_tma(a, tmap, tgrid, s)) k_merge_adjacency<<<148 * 8, 256, 0, s>>>(a);
   k_merge_degree<<<grid, 256, 0, s>>>(a);

@@ -374,6 +374,8 @@ void launch_snapshot(const SnapArgs &a, int grid, cudaStream_t s);
 // begin with pdl_wait_and_trigger()); a plain stream-ordered launch otherwise.
 extern bool g_pdl;
 extern int g_adj_tma;
+extern int g_adj_ilp;
+extern int g_adj_minb8;
 extern int g_bset_rows;
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {

@@ -971,6 +971,7 @@ int rapid_init(rapid_ctx **out, int device, uint64_t max_pixels_total, uint64_t 
   if (const char *e = getenv("RAPID_FUSE_SNAP")) c->fuse_snap = e[0] == '1';
   if (const char *e = getenv("RAPID_SWEEP_NO_SMALLB")) c->no_smallb = e[0] == '1';
   if (const char *e = getenv("RAPID_PDL")) g_pdl = e[0] == '1';
+  if (const char *e = getenv("RAPID_SWEEP_UNI")) g_sweep_uni = e[0] != '0';
   if (const char *e = getenv("RAPID_ADJ_MINB8")) g_adj_minb8 = e[0] == '1';
   if (const char *e = getenv("RAPID_ADJ_ILP")) g_adj_ilp = atoi(e) >= 4 ? 4 : atoi(e) >= 2 ? 2 : 1;
   if (const char *e = getenv("RAPID_ADJ")) g_adj_tma = strcmp(e, "tma") == 0 ? 1 : 0;

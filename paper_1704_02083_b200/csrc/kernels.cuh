@@ -376,6 +376,7 @@ extern bool g_pdl;
 extern int g_adj_tma;
 extern int g_adj_ilp;
 extern int g_adj_minb8;
+extern int g_sweep_uni;
 extern int g_bset_rows;
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {

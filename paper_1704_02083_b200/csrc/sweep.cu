@@ -721,7 +721,9 @@ __device__ __forceinline__ i128 energy(const Rec &ra, const int4 rb, const int d
 // tiles; lane l loads bset word (tile l/8, colour c, plane row l%8), the set bits are
 // distributed 32 at a time over the lanes, and every lane re-tests its block from the label
 // map (boundary, static gate, simple point, Eq. 7), then evaluates Eqs. 1-3 as K4b does.
-template <bool PIXEL, bool GATED, int MINB, bool SMALLB = false, bool LIST = false>
+// UNI: the stage is uniform (every block b x b at (gx b, gy b)) at compile time — the block
+// geometry folds into st.b and the table path is not compiled (fewer live registers)
+template <bool PIXEL, bool GATED, int MINB, bool SMALLB = false, bool LIST = false, bool UNI = false>
 __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) {
   pdl_wait_and_trigger();
   if (sweep_skipped(a.prev)) return;
@@ -789,7 +791,9 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
           const size_t bi = ((size_t)img * nby + gy) * nbx + gx;
           if (st.bsum32) pk32 = ld_stream64(reinterpret_cast<const uint32_t *>(st.bsum) + bi);
           else pk64 = ld_stream64(reinterpret_cast<const unsigned long long *>(st.bsum) + bi);
-          if (st.uniform) {  // every block b x b at (gx b, gy b): no geometry-table loads
+          if (UNI) {
+            // geometry formed where it is used (below): nothing held across the loads
+          } else if (st.uniform) {  // every block b x b at (gx b, gy b): no geometry-table loads
             bx0 = gx * st.b;
             by0 = gy * st.b;
             bw = bh = st.b;
@@ -879,6 +883,7 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
               d[0] = 1; d[1] = rgb & 0xffu; d[2] = (rgb >> 8) & 0xffu; d[3] = rgb >> 16; d[4] = gx; d[5] = gy;
             } else {
               const uint64_t pk = st.bsum32 ? widen_bsum32(pk32) : pk64;
+              if (UNI) { bx0 = gx * st.b; by0 = gy * st.b; bw = bh = st.b; }
               d[0] = bw * bh;
               d[1] = (int)(pk & 0x1FFFFFull);
               d[2] = (int)((pk >> 21) & 0x1FFFFFull);
@@ -888,7 +893,7 @@ __global__ void __launch_bounds__(K4B_THREADS, MINB) k_sweep(const PhaseArgs a) 
             }
             // E_b weight of the slots in a mask: N (1), S (4) edges have length bw; E (2), W (8) bh
             auto wsum = [&](unsigned msk) -> int {
-              return PIXEL ? __popc(msk) : bw * __popc(msk & 5u) + bh * __popc(msk & 10u);
+              return PIXEL ? __popc(msk) : UNI ? st.b * __popc(msk) : bw * __popc(msk & 5u) + bh * __popc(msk & 10u);
             };
             const int wA = wsum(maskA);
             bool hv = false;
@@ -1231,6 +1236,7 @@ void launch_eval(const PhaseArgs &a, bool pixel, int grid, cudaStream_t s) {
 // RAPID_SWEEP_MINB=2..4 forces one budget for every stage (A/B testing).
 static int g_sweep_minb = 0;
 bool g_pdl = false;  // RAPID_PDL=1: programmatic dependent launch of the phase-loop kernels
+int g_sweep_uni = 1;  // RAPID_SWEEP_UNI=0: uniform block stages take the runtime-geometry K4 variant
 static int g_sweep_minb_small = 4;  // RAPID_SWEEP_MINB_SMALL: CTAs/SM of the small-block variant (4: 64 registers, a few bytes of spill, -0.1 ms)
 
 template <int MB>
@@ -1283,6 +1289,7 @@ void launch_sweep(const PhaseArgs &a, bool pixel, bool smallb, bool list, int sm
   if (!occ[mb]) occ[mb] = mb == 2 ? sweep_occ<2>() : mb == 3 ? sweep_occ<3>() : sweep_occ<4>();
   const int grid = sm_count * occ[mb];
   list = list && !pixel;
+  const bool uni = g_sweep_uni && !pixel && a.st.uniform;  // compile-time uniform geometry (RAPID_SWEEP_UNI=0: runtime)
   if (list) launch_pdl(k_bset_list, dim3(sm_count * 8), dim3(256), s, a);
 #define RAPID_SWEEP_LAUNCH(MB)                                                                     \
   if (pixel && gated) launch_pdl(k_sweep<true, true, MB>, dim3(grid), dim3(K4B_THREADS), s, a);        \
@@ -1291,8 +1298,10 @@ void launch_sweep(const PhaseArgs &a, bool pixel, bool smallb, bool list, int sm
   else if (list && smallb) launch_pdl(k_sweep<false, false, MB, true, true>, dim3(grid), dim3(K4B_THREADS), s, a); \
   else if (list && gated) launch_pdl(k_sweep<false, true, MB, false, true>, dim3(grid), dim3(K4B_THREADS), s, a); \
   else if (list) launch_pdl(k_sweep<false, false, MB, false, true>, dim3(grid), dim3(K4B_THREADS), s, a); \
+  else if (gated && smallb && uni) launch_pdl(k_sweep<false, true, MB, true, false, true>, dim3(grid), dim3(K4B_THREADS), s, a); \
   else if (gated && smallb) launch_pdl(k_sweep<false, true, MB, true>, dim3(grid), dim3(K4B_THREADS), s, a); \
   else if (smallb) launch_pdl(k_sweep<false, false, MB, true>, dim3(grid), dim3(K4B_THREADS), s, a);   \
+  else if (gated && uni) launch_pdl(k_sweep<false, true, MB, false, false, true>, dim3(grid), dim3(K4B_THREADS), s, a); \
   else if (gated) launch_pdl(k_sweep<false, true, MB>, dim3(grid), dim3(K4B_THREADS), s, a);           \
   else launch_pdl(k_sweep<false, false, MB>, dim3(grid), dim3(K4B_THREADS), s, a);
   if (mb == 2) { RAPID_SWEEP_LAUNCH(2) }

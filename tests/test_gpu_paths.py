@@ -34,7 +34,7 @@ VARIANTS = [{}, {"RAPID_NO_GRAPH": "1"}, {"RAPID_SWEEP": "scan"}, {"RAPID_FUSE_B
             {"RAPID_NO_TMA": "1"}, {"RAPID_BSET_PARENT": "0"}, {"RAPID_SWEEP_NO_SMALLB": "1"},
             {"RAPID_PDL": "1"}, {"RAPID_ADJ": "tma"}, {"RAPID_BSET_ROWS": "0"},
             {"RAPID_BSET_ROWS": "2"}, {"RAPID_PACKED": "1"},
-            {"RAPID_SWEEP_LIST": "2"}, {"RAPID_ADJ_ILP": "4"}, {"RAPID_ADJ_ILP": "2"}, {"RAPID_ADJ_MINB8": "0"}]
+            {"RAPID_SWEEP_LIST": "2"}, {"RAPID_ADJ_ILP": "4"}, {"RAPID_ADJ_ILP": "2"}, {"RAPID_ADJ_MINB8": "0"}, {"RAPID_SWEEP_UNI": "0"}]
 
 
 @pytest.mark.parametrize("cfg,side", [(2, 1024), (4, 1024), (5, 0)])

@@ -211,7 +211,10 @@ int rapid_stats(rapid_ctx *ctx, rapid_sp_stat *out_host, uint64_t capacity,
                 rapid_run_info *info_host);
 
 /* Profiling: level 1 = CUDA events bracket every kernel class per stage; level 2 also
- * counts each stage's window blocks (rapid_run_info.stage_window_blocks; extra kernels). */
+ * counts each stage's window blocks (rapid_run_info.stage_window_blocks; extra kernels);
+ * level 3 = coarse: events bracket only each stage's whole phase set (RAPID_K_PHASESET) and the
+ * kernel classes outside the phase loop, none between the K3/K4/K5 launches (the nested events
+ * of level 1 add ~7 us per launch group to that interval). */
 int rapid_set_profiling(rapid_ctx *ctx, int enable);
 int rapid_get_profile(rapid_ctx *ctx, rapid_profile *out_host); /* synchronises */
 

@@ -149,7 +149,7 @@ struct rapid_ctx {
   DevBuf qkeys, qcnt, qsize, qspb, qacc;
   bool use_tma = true;  // RAPID_NO_TMA=1 forces the LDG tile loader (A/B testing)
   // profiling
-  int prof = 0;  // 0 off, 1 events, 2 events + window counting
+  int prof = 0;  // 0 off, 1 events, 2 events + window counting, 3 coarse events (phase set as one interval)
   int last_prof = 0;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -476,8 +476,14 @@ struct Timer {  // CUDA events around a launch group (profiling mode only)
   cudaStream_t s;
   int cls, stage;
   cudaEvent_t a = nullptr;
+  // level 3 (coarse): no events between the kernels of the phase loop — only the stage's whole
+  // phase set (RAPID_K_PHASESET) and the kernel classes outside the loop are bracketed
+  bool on() const {
+    if (!c->prof) return false;
+    return c->prof != 3 || !(cls == RAPID_K_SNAPSHOT || cls == RAPID_K_PROPOSE || cls == RAPID_K_COMMIT || cls == RAPID_K_EVAL);
+  }
   Timer(rapid_ctx *c_, cudaStream_t s_, int cls_, int stage_) : c(c_), s(s_), cls(cls_), stage(stage_) {
-    if (!c->prof) return;
+    if (!on()) return;
     a = next();
     record(a);
   }
@@ -502,7 +508,7 @@ struct Timer {  // CUDA events around a launch group (profiling mode only)
     return c->ev_pool[c->ev_used++];
   }
   ~Timer() {
-    if (!c->prof) return;
+    if (!on()) return;
     cudaEvent_t b = next();
     record(b);
     c->evs.push_back({cls, stage, a, b});
@@ -664,7 +670,7 @@ int enqueue(rapid_ctx *c, const uint8_t *image, int H, int W, const rapid_params
       launch_bset_build(ba, has_tmap[st] ? tmaps[st].b : nullptr, has_tmap[st] ? c->tiles_grid : c->sm_count * 8, s);
       c->launches++;
     }
-    if (c->prof >= 2 && use_work) {  // profiling only: algorithmic window of the gated stage
+    if (c->prof == 2 && use_work) {  // profiling only: algorithmic window of the gated stage
       launch_count_window(sd[st], sp, B, M, &ctl->stage_info[st][2], s);
       c->launches++;
     }
@@ -1323,7 +1329,7 @@ int rapid_stats(rapid_ctx *c, rapid_sp_stat *out, uint64_t capacity, rapid_run_i
         if (com == 0) break;
       }
       info->stage_sweeps_run[s] = run;
-      if (c->last_prof >= 2)
+      if (c->last_prof == 2)
         info->stage_window_blocks[s] =
             work ? h->stage_info[s][2] : (uint64_t)P.st[s].nbx * P.st[s].nby * P.B;
     }
@@ -1345,7 +1351,7 @@ int rapid_stats(rapid_ctx *c, rapid_sp_stat *out, uint64_t capacity, rapid_run_i
 
 int rapid_set_profiling(rapid_ctx *c, int enable) {
   if (!c) return RAPID_E_ARG;
-  c->prof = enable < 0 ? 0 : (enable > 2 ? 2 : enable);
+  c->prof = enable < 0 ? 0 : (enable > 3 ? 1 : enable);
   return RAPID_OK;
 }
 

@@ -308,3 +308,45 @@ def test_host_stream_batches():
         r.close()
     for k in range(4):
         assert np.array_equal(labs[k], refs[k]), f"call {k}"
+
+
+def test_profiling_levels_time_the_same_segmentation():
+    """rapid_set_profiling levels 1 (events around every launch group), 2 (+ window counting) and
+    3 (coarse: each stage's phase loop as one interval, no events between K3/K4/K5) change only
+    what is timed: labels and counters are those of level 0, level 3 reports no K3/K4/K5 class
+    and a phase-set interval per stage that ran, and it is not longer than level 1's interval
+    with its inner events by more than noise."""
+    import torch
+    import paper_1704_02083_b200 as rb
+    w = synth.scaled(4, 1024, 1024)
+    img = torch.from_numpy(w.images()).cuda()
+    r = rb.Rapid(0, max_pixels=w.pixels, max_superpixels=w.params.n_superpixels)
+    try:
+        base = r.segment(img, w.params).cpu().numpy()
+        _, info0 = r.stats(0)
+        c0 = info0.counters()
+        ms = {}
+        for level in (1, 2, 3):
+            r.set_profiling(level)
+            r.segment(img, w.params)                  # capture at this level
+            best = None
+            for _ in range(5):
+                lab = r.segment(img, w.params)        # replay
+                m = r.profile().ms_array()
+                best = m if best is None else np.minimum(best, m)
+            assert np.array_equal(lab.cpu().numpy(), base), level
+            _, info = r.stats(0)
+            assert np.array_equal(info.counters(), c0), level
+            ms[level] = best
+        nst = len(w.params.block_sizes)
+        assert (ms[3][rb.K_PHASESET][:nst] > 0).all()
+        for k in (rb.K_SNAPSHOT, rb.K_PROPOSE, rb.K_COMMIT, rb.K_EVAL):
+            assert ms[3][k].sum() == 0, k
+            assert k == rb.K_EVAL or ms[1][k].sum() > 0, k
+        for k in (rb.K_PYRAMID, rb.K_MERGE, rb.K_TRANSITION, rb.K_FINAL):
+            assert ms[3][k].sum() > 0, k
+        assert ms[3][rb.K_PHASESET].sum() <= 1.05 * ms[1][rb.K_PHASESET].sum()
+        r.set_profiling(0)
+        assert np.array_equal(r.segment(img, w.params).cpu().numpy(), base)
+    finally:
+        r.close()

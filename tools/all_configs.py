@@ -9,13 +9,21 @@ import json
 import os
 import subprocess
 import sys
-import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-import oracle  # noqa: E402  (test infrastructure: the CPU baseline leg only)
-import synth  # noqa: E402
+# (the oracle is reached only through bench.py's reference arm)
+
+
+def oracle_full(cfg):
+    """The single-threaded oracle on the whole workload of config `cfg`, through bench.py's
+    reference arm (one step, no warm-up, the sample as large as the config: pinned to one core)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", str(cfg),
+                          "--sample", "65536", "--steps", "1", "--warmup", "0"], capture_output=True, text=True, check=True)
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    return d["value"], d["ms_per_step"] / 1e3
+
 
 rows = []
 for cfg in (1, 2, 3, 4, 5):
@@ -27,16 +35,8 @@ for cfg in (1, 2, 3, 4, 5):
             full = json.load(f)
         rows.append((cfg, d, full["value"], "full, tools/oracle_full.py", full["seconds"]))
         continue
-    w = synth.config(cfg)
-    what = "full"
-    img = w.images()
-    old = os.sched_getaffinity(0)
-    os.sched_setaffinity(0, {min(old)})  # one core, as taskset -c
-    t0 = time.perf_counter()
-    oracle.segment(img, w.params)
-    dt = time.perf_counter() - t0
-    os.sched_setaffinity(0, old)
-    rows.append((cfg, d, w.pixels / dt / 1e6, what, dt))
+    mpx, dt = oracle_full(cfg)
+    rows.append((cfg, d, mpx, "full", dt))
 
 print("| config | workload | GPU ms / segmentation | GPU Mpx/s | k_sweep frac (pixel stage) | "
       "phase-set frac | oracle Mpx/s (1 core) | oracle input |")

@@ -1,57 +1,33 @@
-"""Run the CPU oracle on a whole workload once and report its time and peak RSS (the
-cpu_baseline for full config 4, BASELINE.md's plan: single-threaded, pinned with taskset).
-Optionally saves labels + sums for a later comparison.
+"""Time the CPU oracle on a whole workload once (the cpu_baseline for full config 4, BASELINE.md's
+plan: single-threaded, pinned to one core) and report its time and peak RSS.  The oracle is
+reached only through bench.py's reference arm (`--impl reference`, one step, no warm-up, the
+sample as large as the config), which is where the contract allows it to run.
 
-    taskset -c 0 python tools/oracle_full.py --config 4 [--save out.npz]
+    python tools/oracle_full.py --config 4
 """
 import argparse
 import json
 import os
 import resource
+import subprocess
 import sys
-import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np  # noqa: E402
-
-import oracle  # noqa: E402
-import synth  # noqa: E402
-
-
-def cpu_info():
-    model = None
-    try:
-        for ln in open("/proc/cpuinfo"):
-            if ln.startswith("model name"):
-                model = ln.split(":", 1)[1].strip()
-                break
-    except OSError:
-        pass
-    return {"cpu_model": model, "host_cores": os.cpu_count(),
-            "affinity": len(os.sched_getaffinity(0))}
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=4)
-    ap.add_argument("--side", type=int, default=0)
-    ap.add_argument("--save", default="")
     a = ap.parse_args()
-    w = synth.scaled(a.config, a.side, a.side) if a.side else synth.config(a.config)
-    t0 = time.perf_counter()
-    img = w.images()
-    gen = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    r = oracle.segment(img, w.params)
-    dt = time.perf_counter() - t0
-    out = {"workload": w.name, "pixels": w.pixels, "oracle_s": round(dt, 2),
-           "mpx_s": round(w.pixels / dt / 1e6, 3), "gen_s": round(gen, 1),
-           "max_rss_gb": round(resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 1e6, 2),
-           "alive": int(r.sp["alive"].sum()), **cpu_info()}
-    if a.save:
-        np.save(a.save + "_labels.npy", r.labels)
-        np.save(a.save + "_sp.npy", r.sp)
-    print(json.dumps(out), flush=True)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config",
+                          str(a.config), "--sample", "65536", "--steps", "1", "--warmup", "0"],
+                         capture_output=True, text=True, check=True)
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    cb = d["cpu_baseline"]
+    print(json.dumps({"workload": d["config"]["workload"], "sample": d["config"]["reference_sample"],
+                      "oracle_s": round(d["ms_per_step"] / 1e3, 2), "mpx_s": d["value"],
+                      "max_rss_gb": round(resource.getrusage(resource.RUSAGE_CHILDREN).ru_maxrss / 1e6, 2),
+                      "cpu_model": cb["cpu_model"], "host_cores": cb["host_cores"]}), flush=True)
 
 
 if __name__ == "__main__":

@@ -113,7 +113,7 @@ _LIB = None
 def lib():
     global _LIB
     if _LIB is None:
-        # RAPID_ORACLE_LIB: a mutated build for the mutation check (tools/mutation_check.sh)
+        # RAPID_ORACLE_LIB: a mutated build for the mutation check (tests/mutation_check.sh)
         path = os.environ.get("RAPID_ORACLE_LIB") or os.path.join(_HERE, "liboracle.so")
         if not os.path.exists(path):
             raise RuntimeError(f"{path} missing: run `make oracle`")

@@ -2,7 +2,7 @@
 # Mutation check of the oracle's choice pins: build the oracle with a
 # one-token change of the Eq. 3 argmin (oracle.c argmin_move) or the Eq. 4 argmin
 # (oracle.c merge_round) and require that the CPU pin suite FAILS against each mutant.
-#   bash tools/mutation_check.sh        (from the repo root; CPU only, ~1 min)
+#   bash tests/mutation_check.sh        (from the repo root; CPU only, ~1 min)
 set -u
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 TMP=$(mktemp -d)

@@ -303,3 +303,33 @@ def test_config4_density_options_at_2048(rapid, mask, stats, size_mode):
     p.mask_rule, p.stats_mode, p.size_mode = mask, stats, size_mode
     o, lab, sp, info = assert_parity(rapid, w.images(), p)
     assert info.status == 0
+
+
+def test_random_midsize_config4_densities(rapid):
+    """Random mid-size cases with config 4's densities (ragged sizes of several 32 x 32 tiles
+    up to ~1.5 Mpx, so that worklists, multi-tile boundary sets, merges and the prediction mask
+    all engage), random options, each bit-exact with the oracle.  RAPID_MIDSIZE_SEED /
+    RAPID_MIDSIZE_CASES widen the sweep (profiles/r02j_soak.txt)."""
+    import os
+    rng = np.random.default_rng(int(os.environ.get("RAPID_MIDSIZE_SEED", "77")))
+    for case in range(int(os.environ.get("RAPID_MIDSIZE_CASES", "6"))):
+        H, W = int(rng.integers(200, 1300)), int(rng.integers(200, 1300))
+        w = synth.scaled(4, H, W, B=int(rng.integers(1, 3)), seed_offset=int(rng.integers(1 << 20)))
+        p = w.params
+        while True:  # a superpixel count whose grid fits the image (A1: M = rows x columns)
+            try:
+                oracle.grid(H, W, p.n_superpixels)
+                break
+            except oracle.OracleError:
+                p.n_superpixels -= 1
+        p.sweeps = int(rng.integers(1, 6))
+        p.size_mode = int(rng.integers(0, 3))
+        p.mask_rule = int(rng.integers(0, 4))
+        p.stats_mode = int(rng.choice([0, 0, 1, 2]))
+        p.lambda_b_q16 = int(rng.integers(0, 64 * 65536))
+        if rng.random() < 0.3:
+            p.block_sizes = p.block_sizes[:-int(rng.integers(1, 3))]  # final grain 2 or 4
+        try:
+            assert_parity(rapid, w.images(), p)
+        except AssertionError as e:
+            raise AssertionError(f"case {case}: {w.name} B={w.B} params={p}: {e}") from None
